@@ -1,0 +1,92 @@
+/*
+ * hddm_oracle.h -- CPU restatement of the reference DDM hot path, in C.
+ *
+ * TEST INFRASTRUCTURE ONLY. This is the checker the CUDA engine is compared
+ * against; it is never linked into, called by, or used as a fallback for the
+ * product library (paper_1807_04180_b200/). Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load it.
+ *
+ * Parity is PINNED: tests/test_oracle_vs_ref.py runs this restatement and the
+ * unmodified reference (oracle/_ref/libhelmddm_ref.so, built from
+ * /root/reference/proj/src by oracle/Makefile) on identical inputs, and the
+ * committed fixtures under tests/golden/ (tests/golden/make_golden.py) carry the
+ * reference's outputs to machines without /root/reference.
+ *
+ * Complex arrays are interleaved (re, im) doubles; global fields are row-major,
+ * x fastest, over the dilated global window (proj/include/helmddm/types.hpp:37-56).
+ */
+#ifndef HDDM_ORACLE_H
+#define HDDM_ORACLE_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  double x0, y0, h;
+  int mx, my, n1, n2, n_overlap, n_ramp;
+  double omega;
+  int medium_kind; /* 0 constant, 1 layered, 2 gaussian lens */
+  double velocity; /* constant c, or lens background c0 */
+  int n_layers;
+  const double* layer_ylo;
+  const double* layer_yhi;
+  const double* layer_c;
+  double c_sigma, sigma0;
+  int threads; /* ignored: the restatement is single-threaded */
+  /* lens: c = velocity - lens_amp * exp(-((x-xc)^2 + (y-yc)^2) / lens_w) */
+  double lens_amp, lens_xc, lens_yc, lens_w;
+} orc_problem;
+
+typedef struct {
+  int steps;
+  long solves, skipped;
+  double relres;
+  int converged;
+  double factor_ms, sweep_ms;
+} orc_stats;
+
+typedef struct {
+  int iters;
+  int converged;
+  double relres, true_relres;
+  double wall_ms;
+} orc_fgmres_out;
+
+typedef struct orc_engine orc_engine;
+
+const char* orc_last_error(void);
+int orc_create(const orc_problem* p, orc_engine** out);
+void orc_destroy(orc_engine* e);
+long orc_n_global(const orc_engine* e);
+double orc_sigma0(const orc_engine* e);
+int orc_num_classes(const orc_engine* e);
+int orc_class_info(const orc_engine* e, int c, int* members, long* nnz,
+                   double* probe, int* is_ldlt);
+int orc_class_of(const orc_engine* e, int t);
+int orc_apply_global(const orc_engine* e, const double* u, double* out);
+int orc_solve_iterative(orc_engine* e, const double* f, double tol,
+                        int max_steps, int check_every, double* out,
+                        orc_stats* st, int* hist_step, double* hist_rel,
+                        int hist_cap, int* hist_len);
+int orc_precondition(orc_engine* e, const double* r, double* z, int k,
+                     orc_stats* st);
+int orc_fgmres(orc_engine* e, const double* b, double* x, double tol,
+               int max_iters, int restart, int K, orc_fgmres_out* res,
+               double* hist, int hist_cap, double* zs, int zs_cap,
+               orc_stats* pst);
+/* Debug/parity taps: after precondition(f, K=s) the scaled right-hand side
+ * and solution of subdomain t at step s (window-local natural order). */
+int orc_tap_subdomain(const orc_engine* e, int t, double* rhs, double* u,
+                      int* active);
+/* Solve with class c's factorization (solve_raw + refine semantics). */
+int orc_class_solve(const orc_engine* e, int c, const double* b, double* x,
+                    double* relres);
+/* Window operator coefficient arrays of class c (for kernel unit tests). */
+int orc_window_dims(const orc_engine* e, int* nx, int* ny);
+int orc_nd_order(int nx, int ny, int* order);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
