@@ -1,0 +1,163 @@
+/*
+ * hddm.h -- C-ABI of the B200-native DDM engine (libhddm.so).
+ *
+ * This is the drop-in boundary for the hot path named in BASELINE.json
+ * (north_star): the reference's C++ entry points in proj/include/helmddm/ are
+ * re-expressed as plain C functions over plain pointers and sizes. A header-only
+ * C++ shim (include/helmddm_b200/ddm.hpp) rebuilds the reference's class
+ * surface on top of these functions; INTEGRATION.md shows the bindings.
+ *
+ * Each entry point names the reference interface it replaces. Complex arrays
+ * are interleaved (re, im) doubles (std::complex<double> layout,
+ * proj/include/helmddm/types.hpp:10); global fields are row-major with x fastest
+ * over the dilated global window (types.hpp:37-56), n_global() entries.
+ *
+ * memkind: HDDM_HOST -> caller pointers are host memory (the engine copies
+ * through pinned staging and synchronises before returning);
+ * HDDM_DEVICE -> pointers are device memory on the engine's device, work is
+ * ordered on the engine's stream and the call still synchronises before
+ * returning (statistics are host values).
+ *
+ * Return codes mirror the reference CLI (proj/src/cli.cpp:453-469):
+ * 0 ok, 2 configuration error (ConfigError), 3 solve error (SolveError),
+ * 1 any other error (CUDA failure, std::domain_error, ...).
+ * There is NO CPU fallback: without a usable CUDA device hddm_create fails.
+ */
+#ifndef HDDM_H
+#define HDDM_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HDDM_HOST 0
+#define HDDM_DEVICE 1
+
+#define HDDM_OK 0
+#define HDDM_ERR_OTHER 1
+#define HDDM_ERR_CONFIG 2
+#define HDDM_ERR_SOLVE 3
+
+#define HDDM_MEDIUM_CONSTANT 0
+#define HDDM_MEDIUM_LAYERED 1
+#define HDDM_MEDIUM_LENS 2
+
+/* DdmConfig (proj/include/helmddm/ddm.hpp:15-22) flattened: GridSpec
+ * (partition.hpp:13-31) + MediumModel (medium.hpp:17-29) + c_sigma/sigma0.
+ * medium_kind LENS is this repo's extension (BASELINE config 3):
+ * c(x,y) = velocity - lens_amp * exp(-((x-lens_xc)^2 + (y-lens_yc)^2) / lens_w)
+ * with (x, y) clamped into the interior box. */
+typedef struct hddm_problem_s {
+  double x0, y0, h;
+  int mx, my, n1, n2, n_overlap, n_ramp;
+  double omega;
+  int medium_kind;
+  double velocity;
+  int n_layers;
+  const double* layer_ylo;
+  const double* layer_yhi;
+  const double* layer_c;
+  double c_sigma, sigma0;
+  int threads; /* accepted for DdmConfig parity; unused (the GPU replaces WorkerPool) */
+  double lens_amp, lens_xc, lens_yc, lens_w;
+  int device; /* CUDA device ordinal */
+} hddm_problem;
+
+/* DdmStats (ddm.hpp:30-39) without the history vector (returned separately). */
+typedef struct {
+  int steps;
+  long solves, skipped;
+  double relres;
+  int converged;
+  double factor_ms, sweep_ms;
+} hddm_stats;
+
+/* FgmresResult (krylov.hpp:18-25) without the vectors. */
+typedef struct {
+  int iters;
+  int converged;
+  double relres, true_relres;
+  double wall_ms;
+} hddm_fgmres_result;
+
+typedef struct hddm_engine hddm_engine;
+
+/* Last error message of the calling thread (create failures) or of engine e. */
+const char* hddm_last_error(const hddm_engine* e);
+
+/* DdmEngine::DdmEngine(const DdmConfig&)  -- ddm.hpp:55, ddm.cpp:62-101.
+ * Host setup (partition, coefficients, classes, symbolic analysis), then the
+ * batched numeric LDL^T of every class on the GPU and its probe solve
+ * (sparse.cpp:203-236). A probe residual above 1e-10 is a SolveError (3):
+ * there is no LU fallback. */
+int hddm_create(const hddm_problem* p, hddm_engine** out);
+void hddm_destroy(hddm_engine* e);
+
+/* Accessors -- ddm.hpp:57-63 */
+long hddm_n_global(const hddm_engine* e);
+double hddm_sigma0(const hddm_engine* e);
+double hddm_factor_ms(const hddm_engine* e);
+int hddm_num_subdomains(const hddm_engine* e);
+int hddm_num_classes(const hddm_engine* e);
+/* OpClassInfo (ddm.hpp:41-46): members, factor_nonzeros() as the reference
+ * counts it (nnz(L)+n), probe_relres, backend ("ldlt" -> 1). */
+int hddm_class_info(const hddm_engine* e, int c, int* members, long* nnz,
+                    double* probe_relres, int* is_ldlt);
+int hddm_class_of(const hddm_engine* e, int t);
+
+/* DdmEngine::apply_global(const Complex* u, Complex* out) -- ddm.hpp:66 */
+int hddm_apply_global(hddm_engine* e, const double* u, double* out, int memkind);
+
+/* DdmEngine::solve_iterative(f, tol, max_steps, stats, check_every) --
+ * ddm.hpp:72-74, ddm.cpp:244-278. out receives the assembled global field.
+ * hist_* (may be NULL) receive the evaluated (step, relres, wall_ms). */
+int hddm_solve_iterative(hddm_engine* e, const double* f, double tol,
+                         int max_steps, int check_every, double* out,
+                         int memkind, hddm_stats* stats, int* hist_step,
+                         double* hist_rel, double* hist_ms, int hist_cap,
+                         int* hist_len);
+
+/* DdmEngine::precondition(r, z, ksteps, stats) -- ddm.hpp:78, ddm.cpp:280-287.
+ * Solve counts and sweep time ACCUMULATE into *stats (as the reference). */
+int hddm_precondition(hddm_engine* e, const double* r, double* z, int ksteps,
+                      int memkind, hddm_stats* stats);
+
+/* fgmres(n, A=apply_global, M=precondition(K), b, x, opt) -- krylov.hpp:31-33
+ * wired as proj/src/cli.cpp:210-228; restart 0 = no restart. Device-resident:
+ * V, Z, H, Givens state never leave HBM. hist (may be NULL) receives the
+ * recursive relres per iteration; pstats accumulates preconditioner stats. */
+int hddm_fgmres(hddm_engine* e, const double* b, double* x, double tol,
+                int max_iters, int restart, int ksteps, int memkind,
+                hddm_fgmres_result* res, double* hist, int hist_cap,
+                hddm_stats* pstats);
+
+/* ---- parity / measurement taps (not part of the reference surface) ---- */
+
+/* After the last sweep: subdomain t's scaled right-hand side and solution in
+ * window-local natural order (n_w complex each) and its active flag. */
+int hddm_tap_subdomain(hddm_engine* e, int t, double* rhs, double* u,
+                       int* active);
+/* Solve A_c x = b with class c's factors (window-local natural order,
+ * host memory); relres = ||b - A x|| / ||b|| as refine() reports it. */
+int hddm_class_solve(hddm_engine* e, int c, const double* b, double* x,
+                     double* relres);
+/* Window node counts and the reference elimination order (perm[pos] = node). */
+int hddm_window_dims(const hddm_engine* e, int* nx, int* ny);
+int hddm_nd_order(int nx, int ny, int* order);
+/* Symbolic/footprint figures: stored factor values per class, the
+ * reference's nnz(L)+n per class, total device bytes held by the engine. */
+int hddm_footprint(const hddm_engine* e, long* stored_per_class,
+                   long* ref_nnz_per_class, long* device_bytes);
+/* Run K DDM steps of the preconditioner on device vectors without
+ * synchronising (bench helper); per-kernel-kind device times (ms) of the last
+ * call can be read with hddm_stage_times when timing was enabled. */
+int hddm_set_timing(hddm_engine* e, int enable);
+int hddm_stage_times(const hddm_engine* e, double* ms, int cap, int* n);
+const char* hddm_stage_name(int i);
+/* CUDA stream (cudaStream_t) the engine orders its work on. */
+void* hddm_stream(const hddm_engine* e);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,84 @@
+// Device-side helpers and POD tables shared by the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace hddm {
+
+typedef double2 cplx;
+
+__host__ __device__ __forceinline__ cplx cmk(double r, double i) { return make_double2(r, i); }
+__host__ __device__ __forceinline__ cplx cadd(cplx a, cplx b) { return cmk(a.x + b.x, a.y + b.y); }
+__host__ __device__ __forceinline__ cplx csub(cplx a, cplx b) { return cmk(a.x - b.x, a.y - b.y); }
+__host__ __device__ __forceinline__ cplx cmul(cplx a, cplx b) {
+  return cmk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__host__ __device__ __forceinline__ cplx cscale(cplx a, double s) { return cmk(a.x * s, a.y * s); }
+__host__ __device__ __forceinline__ cplx cconj(cplx a) { return cmk(a.x, -a.y); }
+__host__ __device__ __forceinline__ double cnorm2(cplx a) { return a.x * a.x + a.y * a.y; }
+// acc += a * b
+__device__ __forceinline__ void cfma(cplx& acc, cplx a, cplx b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+// a / b (operands here are O(1)..O(1e8) pivots/Jacobians; no overflow scaling)
+__host__ __device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
+  const double d = b.x * b.x + b.y * b.y;
+  return cmk((a.x * b.x + a.y * b.y) / d, (a.y * b.x - a.x * b.y) / d);
+}
+__device__ __forceinline__ cplx shfl_xor(cplx v, int m) {
+  return cmk(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
+}
+__device__ __forceinline__ cplx warp_sum(cplx v) {
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) v = cadd(v, shfl_xor(v, m));
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+  return v;
+}
+__device__ __forceinline__ cplx ldg(const cplx* p) { return __ldg(p); }
+
+// ------------------------------------------------------------ device tables
+struct DevSn {
+  int kind, c0, n, nrows;
+  int blk0, nblk, drow0, parent;
+  int child0, child1, extadd0, aent0;
+  int aent1, pad0;
+  long long diag_off, dinv_off, front_off;
+};
+
+struct DevBlk {
+  int src, dst, r0, nr, row0, front0;
+};
+
+// one solve task: supernode s, rows/columns [a, b)
+struct Task {
+  int s, a, b, pad;
+};
+
+// incoming forward entry for one separator row: profile row of a descendant
+struct RowIn {
+  int rowtab, src_c0, src_n, pad;
+};
+
+struct DevSub {
+  int i, j, cx0, cx1, cy0, cy1, wx0, wy0;
+  int lint, rint, bint, tint;
+  int own0, own1, own2, own3;
+  int cls, pad0, pad1, pad2;
+};
+
+// quintic taper beta0, proj/src/partition.cpp:7-11
+__host__ __device__ __forceinline__ double beta0(double t) {
+  if (t <= 0) return 1.0;
+  if (t >= 1) return 0.0;
+  return 1.0 - t * t * t * (10.0 - 15.0 * t + 6.0 * t * t);
+}
+
+}  // namespace hddm

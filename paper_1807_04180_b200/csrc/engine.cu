@@ -1,0 +1,1149 @@
+// B200 DDM engine: host orchestration + the C-ABI of include/hddm.h.
+//
+// DdmEngine (proj/include/helmddm/ddm.hpp:53-109) re-designed for one GPU:
+//   * host: setup (setup.cpp) and symbolic analysis (symbolic.cpp), once;
+//   * device: batched multifrontal factorization of every class, then each DDM
+//     step is  flags -> gather-sources -> batched supernodal solves ->
+//     residual check -> blend-accumulate, all HBM-resident on one stream;
+//   * FGMRES keeps V, Z, H, Givens and g on the device.
+// There is no CPU fallback: every numeric stage is a CUDA kernel; without a
+// CUDA device hddm_create fails.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <complex>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "hddm.h"
+#include "hddm_internal.h"
+#include "kernels.cuh"
+#include "kernels_krylov.cuh"
+
+using namespace hddm;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct SolveErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ConfigErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CK(x)                                                                        \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess)                                                           \
+      throw std::runtime_error(std::string("CUDA error: ") + cudaGetErrorString(e_) + \
+                               " at " + __FILE__ + ":" + std::to_string(__LINE__));  \
+  } while (0)
+
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+const char* kStageNames[] = {"flags+gather", "solve", "check", "accumulate", "global_apply",
+                             "krylov"};
+constexpr int kStages = 6;
+
+}  // namespace
+
+struct hddm_engine {
+  Setup S;
+  Symbolic Y;
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  std::string err;
+  int nsub = 0, ncls = 0, nw = 0, wnx = 0, wny = 0, max_members = 0;
+  long long ng = 0;
+  double factor_ms = 0;
+  std::vector<double> probe;
+  size_t dev_bytes = 0;
+  std::vector<void*> allocs;
+  int last_step = 0;
+  bool timing = false;
+  cudaEvent_t ev[2 * kStages] = {};
+  double stage_ms[kStages] = {};
+
+  // symbolic tables
+  DevSn* d_sn = nullptr;
+  DevBlk* d_blk = nullptr;
+  int* d_row_first = nullptr;
+  long long* d_row_off = nullptr;
+  int* d_rin_ptr = nullptr;
+  RowIn* d_rin = nullptr;
+  int* d_perm = nullptr;
+  int* d_pinv = nullptr;
+  SolvePlan plan;
+  cplx* d_vals = nullptr;
+  // per subdomain
+  DevSub* d_sub = nullptr;
+  cplx* d_sa = nullptr;
+  int sa_stride = 0;
+  double* d_wx = nullptr;
+  double* d_wy = nullptr;
+  cplx* d_U[3] = {};
+  cplx* d_B = nullptr;
+  cplx* d_Y = nullptr;
+  int* d_Z[3] = {};
+  int* d_fany = nullptr;
+  int* d_cls_ptr = nullptr;
+  int* d_cls_mem = nullptr;
+  int* d_act_ptr = nullptr;
+  int* d_act_list = nullptr;
+  long long* d_counts = nullptr;
+  double* d_part_chk = nullptr;
+  int nchunk = 8;
+  double* d_rel = nullptr;
+  int* d_refine = nullptr;
+  double* d_maxrel = nullptr;
+  // global
+  cplx* d_ga = nullptr;
+  double* d_k2 = nullptr;
+  cplx* d_f = nullptr;
+  cplx* d_asm = nullptr;
+  cplx* d_tmp = nullptr;
+  int* d_colcov = nullptr;
+  int* d_rowcov = nullptr;
+  double* d_part = nullptr;
+  double* d_scal = nullptr;  // small scalars
+  double* h_scal = nullptr;  // pinned mirror
+  // krylov
+  int kry_m = 0;
+  std::vector<cplx*> V, Z;
+  cplx** d_Zptr = nullptr;
+  cplx* d_H = nullptr;
+  cplx* d_g = nullptr;
+  cplx* d_sn_g = nullptr;
+  double* d_cs = nullptr;
+  cplx* d_y = nullptr;
+  cplx* d_b = nullptr;
+  cplx* d_x = nullptr;
+  cplx* d_r = nullptr;
+
+  template <class T>
+  T* dalloc(size_t n) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    allocs.push_back(p);
+    dev_bytes += std::max<size_t>(n, 1) * sizeof(T);
+    return static_cast<T*>(p);
+  }
+  void dfree(void* p) {
+    auto it = std::find(allocs.begin(), allocs.end(), p);
+    if (it != allocs.end()) allocs.erase(it);
+    cudaFree(p);
+  }
+  template <class T>
+  T* upload(const std::vector<T>& v) {
+    T* p = dalloc<T>(v.size());
+    if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    return p;
+  }
+
+  ~hddm_engine() {
+    if (dev >= 0) cudaSetDevice(dev);
+    for (void* p : allocs) cudaFree(p);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (h_scal) cudaFreeHost(h_scal);
+    if (st) cudaStreamDestroy(st);
+  }
+
+  void create(const hddm_problem& p);
+  void factorize();
+  void run_probe();
+  StepArgs step_args(int s, const cplx* f);
+  SolveArgs solve_args(const cplx* B, cplx* X, cplx* Y);
+  void enqueue_step(int s, const cplx* f);
+  void reset_state();
+  void fill_flags(int* p, int v, int n);
+  double device_norm(const cplx* v);
+  void stage_begin(int k) {
+    if (timing) CK(cudaEventRecord(ev[2 * k], st));
+  }
+  void stage_end(int k) {
+    if (timing) CK(cudaEventRecord(ev[2 * k + 1], st));
+  }
+  void stage_collect(int k) {
+    if (!timing) return;
+    float ms = 0;
+    CK(cudaEventSynchronize(ev[2 * k + 1]));
+    CK(cudaEventElapsedTime(&ms, ev[2 * k], ev[2 * k + 1]));
+    stage_ms[k] += ms;
+  }
+  void ensure_krylov(int m);
+};
+
+// ----------------------------------------------------------------- creation
+void hddm_engine::create(const hddm_problem& p) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw std::runtime_error("no CUDA device available (the engine has no CPU fallback)");
+  dev = p.device;
+  if (dev < 0 || dev >= ndev) throw ConfigErr("invalid CUDA device ordinal");
+  CK(cudaSetDevice(dev));
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  CK(cudaMallocHost(&h_scal, 64 * sizeof(double)));
+  std::string msg;
+  const int rc = build_setup(p, S, msg);
+  if (rc == HDDM_ERR_CONFIG) throw ConfigErr(msg);
+  if (rc) throw std::runtime_error(msg);
+  nsub = S.n1 * S.n2;
+  ncls = S.ncls;
+  wnx = S.subs[0].nx;
+  wny = S.subs[0].ny;
+  nw = wnx * wny;
+  ng = (long long)S.gnx * S.gny;
+  for (int c = 0; c < ncls; ++c)
+    max_members = std::max(max_members, S.cls_ptr[c + 1] - S.cls_ptr[c]);
+  build_symbolic(wnx, wny, Y);
+
+  // ---- symbolic tables
+  std::vector<DevSn> sn(Y.sn.size());
+  for (size_t s = 0; s < Y.sn.size(); ++s) {
+    const SnNode& a = Y.sn[s];
+    DevSn& d = sn[s];
+    d.kind = a.kind;
+    d.c0 = a.c0;
+    d.n = a.n;
+    d.nrows = int(a.rows.size());
+    d.blk0 = a.blk0;
+    d.nblk = a.nblk;
+    d.drow0 = a.drow0;
+    d.parent = a.parent;
+    d.child0 = a.nch > 0 ? a.child[0] : -1;
+    d.child1 = a.nch > 1 ? a.child[1] : -1;
+    d.extadd0 = a.extadd0;
+    d.aent0 = Y.aent0[s];
+    d.aent1 = Y.aent0[s + 1];
+    d.diag_off = a.diag_off;
+    d.dinv_off = a.dinv_off;
+    d.front_off = a.front_off;
+  }
+  d_sn = upload(sn);
+  std::vector<DevBlk> blk(Y.blk.size());
+  for (size_t b = 0; b < Y.blk.size(); ++b) {
+    const Block& a = Y.blk[b];
+    blk[b] = {a.src, a.dst, a.r0, a.nr, a.row0, a.front0};
+  }
+  d_blk = upload(blk);
+  d_row_first = upload(Y.row_first);
+  std::vector<long long> roff(Y.row_off.begin(), Y.row_off.end());
+  d_row_off = upload(roff);
+  d_perm = upload(Y.perm);
+  d_pinv = upload(Y.pinv);
+  // incoming forward entries per separator row (fixed order: block index)
+  {
+    std::vector<std::vector<RowIn>> per(nw);
+    for (size_t b = 0; b < Y.blk.size(); ++b) {
+      const Block& B = Y.blk[b];
+      const SnNode& src = Y.sn[B.src];
+      for (int r = 0; r < B.nr; ++r) {
+        const int rt = B.row0 + r;
+        if (Y.row_first[rt] >= src.n) continue;
+        per[Y.sn[B.dst].c0 + B.r0 + r].push_back({rt, src.c0, src.n, 0});
+      }
+    }
+    std::vector<int> ptr(nw + 1, 0);
+    std::vector<RowIn> all;
+    for (int k = 0; k < nw; ++k) {
+      ptr[k] = int(all.size());
+      all.insert(all.end(), per[k].begin(), per[k].end());
+    }
+    ptr[nw] = int(all.size());
+    d_rin_ptr = upload(ptr);
+    d_rin = upload(all);
+  }
+  // solve plan: leaves; forward levels by height; backward levels by depth
+  {
+    std::vector<int> leaves;
+    for (size_t s = 0; s < Y.sn.size(); ++s)
+      if (Y.sn[s].kind == 0) leaves.push_back(int(s));
+    plan.nleaf = int(leaves.size());
+    plan.d_leaves = upload(leaves);
+    const int R = 8, C = 256;
+    for (int h = 1; h <= Y.max_height; ++h) {
+      std::vector<Task> t;
+      for (size_t s = 0; s < Y.sn.size(); ++s)
+        if (Y.sn[s].kind == 1 && Y.sn[s].height == h)
+          for (int a = 0; a < Y.sn[s].n; a += R) t.push_back({int(s), a, std::min(a + R, Y.sn[s].n), 0});
+      if (t.empty()) continue;
+      SolveLevel L;
+      L.ntask = int(t.size());
+      L.d_tasks = upload(t);
+      plan.fwd.push_back(L);
+    }
+    for (int d = 0; d <= Y.max_depth; ++d) {
+      std::vector<Task> t;
+      for (size_t s = 0; s < Y.sn.size(); ++s)
+        if (Y.sn[s].kind == 1 && Y.sn[s].depth == d)
+          for (int a = 0; a < Y.sn[s].n; a += C) t.push_back({int(s), a, std::min(a + C, Y.sn[s].n), 0});
+      if (t.empty()) continue;
+      SolveLevel L;
+      L.ntask = int(t.size());
+      L.d_tasks = upload(t);
+      plan.bwd.push_back(L);
+    }
+  }
+
+  // ---- per-subdomain data
+  std::vector<DevSub> subs(nsub);
+  sa_stride = 2 * wnx + 2 * wny;
+  std::vector<cplx> sa(size_t(nsub) * sa_stride);
+  std::vector<double> wx(size_t(nsub) * wnx), wy(size_t(nsub) * wny);
+  for (int t = 0; t < nsub; ++t) {
+    const Sub& s = S.subs[t];
+    DevSub& d = subs[t];
+    d.i = s.i;
+    d.j = s.j;
+    d.cx0 = s.cx0;
+    d.cx1 = s.cx1;
+    d.cy0 = s.cy0;
+    d.cy1 = s.cy1;
+    d.wx0 = s.wx0;
+    d.wy0 = s.wy0;
+    d.lint = s.lint;
+    d.rint = s.rint;
+    d.bint = s.bint;
+    d.tint = s.tint;
+    d.own0 = s.own[0];
+    d.own1 = s.own[1];
+    d.own2 = s.own[2];
+    d.own3 = s.own[3];
+    d.cls = s.cls;
+    const WinOp& w = S.subop[t];
+    cplx* o = &sa[size_t(t) * sa_stride];
+    for (int k = 0; k < wnx; ++k) {
+      o[k] = cmk(w.a1n[2 * k], w.a1n[2 * k + 1]);
+      o[wnx + k] = cmk(w.ia1h[2 * k], w.ia1h[2 * k + 1]);
+    }
+    for (int k = 0; k < wny; ++k) {
+      o[2 * wnx + k] = cmk(w.a2n[2 * k], w.a2n[2 * k + 1]);
+      o[2 * wnx + wny + k] = cmk(w.ia2h[2 * k], w.ia2h[2 * k + 1]);
+    }
+    std::copy(s.wx.begin(), s.wx.end(), wx.begin() + size_t(t) * wnx);
+    std::copy(s.wy.begin(), s.wy.end(), wy.begin() + size_t(t) * wny);
+  }
+  d_sub = upload(subs);
+  d_sa = upload(sa);
+  d_wx = upload(wx);
+  d_wy = upload(wy);
+  d_cls_ptr = upload(S.cls_ptr);
+  d_cls_mem = upload(S.cls_members);
+  for (int k = 0; k < 3; ++k) {
+    d_U[k] = dalloc<cplx>(size_t(nsub) * nw);
+    d_Z[k] = dalloc<int>(nsub);
+  }
+  d_B = dalloc<cplx>(size_t(nsub) * nw);
+  d_Y = dalloc<cplx>(size_t(nsub) * nw);
+  CK(cudaMemsetAsync(d_B, 0, size_t(nsub) * nw * sizeof(cplx), st));
+  d_fany = dalloc<int>(nsub);
+  d_act_ptr = dalloc<int>(ncls + 1);
+  d_act_list = dalloc<int>(nsub);
+  d_counts = dalloc<long long>(2);
+  d_part_chk = dalloc<double>(size_t(nsub) * nchunk * 2);
+  d_rel = dalloc<double>(nsub);
+  d_refine = dalloc<int>(1);
+  d_maxrel = dalloc<double>(1);
+
+  // ---- global data
+  std::vector<cplx> ga(size_t(2) * S.gnx + 2 * S.gny);
+  for (int k = 0; k < S.gnx; ++k) {
+    ga[k] = cmk(S.gop.a1n[2 * k], S.gop.a1n[2 * k + 1]);
+    ga[S.gnx + k] = cmk(S.gop.ia1h[2 * k], S.gop.ia1h[2 * k + 1]);
+  }
+  for (int k = 0; k < S.gny; ++k) {
+    ga[2 * S.gnx + k] = cmk(S.gop.a2n[2 * k], S.gop.a2n[2 * k + 1]);
+    ga[2 * S.gnx + S.gny + k] = cmk(S.gop.ia2h[2 * k], S.gop.ia2h[2 * k + 1]);
+  }
+  d_ga = upload(ga);
+  d_k2 = upload(S.k2);
+  d_f = dalloc<cplx>(ng);
+  d_asm = dalloc<cplx>(ng);
+  d_tmp = dalloc<cplx>(ng);
+  // blend coverage per global column / row (accumulate region, ddm.cpp:221-224)
+  {
+    std::vector<int> colcov(size_t(4) * S.gnx, -1), rowcov(size_t(4) * S.gny, -1);
+    for (int i = 0; i < S.n1; ++i) {
+      const Sub& s = S.subs[i];
+      const int x0 = s.lint ? s.cx0 - S.nov : s.wx0;
+      const int x1 = s.rint ? s.cx1 + S.nov : s.wx0 + s.nx - 1;
+      for (int P = x0; P <= x1; ++P) {
+        int k = 0;
+        while (k < 4 && colcov[4 * P + k] >= 0) ++k;
+        if (k == 4) throw ConfigErr("more than 4 overlapping subdomains per column");
+        colcov[4 * P + k] = i;
+      }
+    }
+    for (int j = 0; j < S.n2; ++j) {
+      const Sub& s = S.subs[size_t(j) * S.n1];
+      const int y0 = s.bint ? s.cy0 - S.nov : s.wy0;
+      const int y1 = s.tint ? s.cy1 + S.nov : s.wy0 + s.ny - 1;
+      for (int Q = y0; Q <= y1; ++Q) {
+        int k = 0;
+        while (k < 4 && rowcov[4 * Q + k] >= 0) ++k;
+        if (k == 4) throw ConfigErr("more than 4 overlapping subdomains per row");
+        rowcov[4 * Q + k] = j;
+      }
+    }
+    d_colcov = upload(colcov);
+    d_rowcov = upload(rowcov);
+  }
+  d_part = dalloc<double>(2 * size_t(reduce_blocks()));
+  d_scal = dalloc<double>(64);
+
+  factorize();
+  run_probe();
+}
+
+// ----------------------------------------------------------------- factorization
+void hddm_engine::factorize() {
+  const auto t0 = now_ms();
+  const int naent = int(Y.aent_i.size());
+  // matrix entries per class in front coordinates (assemble, discretize.cpp:131-158)
+  std::vector<cplx> aval(size_t(ncls) * naent);
+  const double ih2 = 1.0 / (S.h * S.h);
+  using cd = std::complex<double>;
+  for (int c = 0; c < ncls; ++c) {
+    const int t = S.cls_rep[c];
+    const Sub& sb = S.subs[t];
+    const WinOp& w = S.subop[t];
+    auto C = [](const std::vector<double>& v, int k) { return cd(v[2 * k], v[2 * k + 1]); };
+    for (int e = 0; e < naent; ++e) {
+      const int v = Y.aent_node[e];
+      const int lp = v % wnx, lq = v / wnx;
+      const cd ew = C(w.a2n, lq) * C(w.ia1h, lp - 1) * ih2;
+      const cd ee = C(w.a2n, lq) * C(w.ia1h, lp) * ih2;
+      const cd es = C(w.a1n, lp) * C(w.ia2h, lq - 1) * ih2;
+      const cd en = C(w.a1n, lp) * C(w.ia2h, lq) * ih2;
+      cd val;
+      switch (Y.aent_kind[e]) {
+        case 0: {
+          const double k2 = S.k2[size_t(sb.wy0 + lq) * S.gnx + sb.wx0 + lp];
+          val = -(ew + ee + es + en) + k2 * (C(w.a1n, lp) * C(w.a2n, lq));
+          break;
+        }
+        case 1: val = ew; break;
+        case 2: val = ee; break;
+        case 3: val = es; break;
+        default: val = en; break;
+      }
+      aval[size_t(c) * naent + e] = cmk(val.real(), val.imag());
+    }
+  }
+  cplx* d_aval = upload(aval);
+  std::vector<int> aent_i = Y.aent_i, aent_j = Y.aent_j;
+  int* d_ai = upload(aent_i);
+  int* d_aj = upload(aent_j);
+  int* d_ext = upload(Y.extadd);
+  d_vals = dalloc<cplx>(size_t(ncls) * Y.nvals);
+  CK(cudaMemsetAsync(d_vals, 0, size_t(ncls) * Y.nvals * sizeof(cplx), st));
+  int* d_status = dalloc<int>(ncls);
+  CK(cudaMemsetAsync(d_status, 0, sizeof(int) * ncls, st));
+  // class batches bounded by ~8 GB of front workspace
+  const size_t per = size_t(Y.front_words) * sizeof(cplx);
+  const int batch = std::max(1, int(std::min<size_t>(ncls, (size_t(8) << 30) / per)));
+  cplx* d_front = dalloc<cplx>(size_t(batch) * Y.front_words);
+  // nodes by height
+  std::vector<std::vector<int>> lev(Y.max_height + 1);
+  for (size_t s = 0; s < Y.sn.size(); ++s) lev[Y.sn[s].height].push_back(int(s));
+  std::vector<int*> d_lev;
+  for (auto& l : lev) d_lev.push_back(upload(l));
+  for (int c0 = 0; c0 < ncls; c0 += batch) {
+    const int nb = std::min(batch, ncls - c0);
+    FactorArgs A;
+    A.sn = d_sn;
+    A.blk = d_blk;
+    A.row_first = d_row_first;
+    A.row_off = d_row_off;
+    A.extadd = d_ext;
+    A.aent_i = d_ai;
+    A.aent_j = d_aj;
+    A.aval = d_aval + size_t(c0) * naent;
+    A.naent = naent;
+    A.front = d_front;
+    A.front_words = Y.front_words;
+    A.vals = d_vals + size_t(c0) * Y.nvals;
+    A.nvals = Y.nvals;
+    A.status = d_status + c0;
+    for (size_t h = 0; h < lev.size(); ++h)
+      if (!lev[h].empty()) launch_factor_level(A, d_lev[h], int(lev[h].size()), nb, st);
+    CK(cudaGetLastError());
+  }
+  std::vector<int> status(ncls);
+  CK(cudaMemcpyAsync(status.data(), d_status, sizeof(int) * ncls, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int c = 0; c < ncls; ++c)
+    if (status[c]) throw SolveErr("LDL^T breakdown (zero pivot); no LU fallback on the GPU path");
+  for (int* p : d_lev) dfree(p);
+  dfree(d_front);
+  dfree(d_aval);
+  dfree(d_ai);
+  dfree(d_aj);
+  dfree(d_ext);
+  dfree(d_status);
+  factor_ms = now_ms() - t0;
+}
+
+SolveArgs hddm_engine::solve_args(const cplx* Bp, cplx* X, cplx* Yp) {
+  SolveArgs A;
+  A.sn = d_sn;
+  A.blk = d_blk;
+  A.row_first = d_row_first;
+  A.row_off = d_row_off;
+  A.rin_ptr = d_rin_ptr;
+  A.rin = d_rin;
+  A.vals = d_vals;
+  A.nvals = Y.nvals;
+  A.act_ptr = d_act_ptr;
+  A.act_list = d_act_list;
+  A.B = Bp;
+  A.X = X;
+  A.Y = Yp;
+  A.nw = nw;
+  A.nring = Y.nring;
+  return A;
+}
+
+// probe solve per class (Factorization::factor, sparse.cpp:215-235)
+void hddm_engine::run_probe() {
+  std::vector<cplx> bnat(nw);
+  uint64_t s = 0x9E3779B97F4A7C15ull;
+  auto next = [&s] {
+    s = s * 6364136223846793005ull + 1442695040888963407ull;
+    return double(s >> 11) * 0x1.0p-52 - 1.0;
+  };
+  for (int i = 0; i < nw; ++i) {
+    const double re = next();
+    bnat[i] = cmk(re, next());
+  }
+  std::vector<cplx> bfo(nw);
+  for (int k = 0; k < nw; ++k) bfo[k] = bnat[Y.perm[k]];
+  std::vector<int> zc(nsub, 1), aptr(ncls + 1), alist(ncls);
+  for (int c = 0; c < ncls; ++c) {
+    const int t = S.cls_rep[c];
+    zc[t] = 0;
+    aptr[c] = c;
+    alist[c] = t;
+    CK(cudaMemcpyAsync(d_B + size_t(t) * nw, bfo.data(), nw * sizeof(cplx), cudaMemcpyHostToDevice, st));
+  }
+  aptr[ncls] = ncls;
+  CK(cudaMemcpyAsync(d_Z[0], zc.data(), sizeof(int) * nsub, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_act_ptr, aptr.data(), sizeof(int) * (ncls + 1), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_act_list, alist.data(), sizeof(int) * ncls, cudaMemcpyHostToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  launch_solve(solve_args(d_B, d_U[0], d_Y), plan, ncls, 1, st);
+  CheckArgs C;
+  C.nw = nw;
+  C.wnx = wnx;
+  C.wny = wny;
+  C.gnx = S.gnx;
+  C.nring = Y.nring;
+  C.ih2 = 1.0 / (S.h * S.h);
+  C.sub = d_sub;
+  C.sa = d_sa;
+  C.sa_stride = sa_stride;
+  C.k2 = d_k2;
+  C.perm = d_perm;
+  C.pinv = d_pinv;
+  C.zc = d_Z[0];
+  C.nsub = nsub;
+  C.B = d_B;
+  C.X = d_U[0];
+  C.part = d_part_chk;
+  C.nchunk = nchunk;
+  C.rel = d_rel;
+  C.refine_flag = d_refine;
+  C.max_rel = d_maxrel;
+  CK(cudaMemsetAsync(d_refine, 0, sizeof(int), st));
+  CK(cudaMemsetAsync(d_maxrel, 0, sizeof(double), st));
+  launch_check(C, st);
+  CK(cudaGetLastError());
+  std::vector<double> rel(nsub);
+  CK(cudaMemcpyAsync(rel.data(), d_rel, sizeof(double) * nsub, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  probe.assign(ncls, 0);
+  for (int c = 0; c < ncls; ++c) {
+    probe[c] = rel[S.cls_rep[c]];
+    if (!(probe[c] <= 1e-10))
+      throw SolveErr("LDL^T probe residual above 1e-10 (class " + std::to_string(c) +
+                     "); no LU fallback on the GPU path");
+  }
+}
+
+// ----------------------------------------------------------------- DDM step
+StepArgs hddm_engine::step_args(int s, const cplx* f) {
+  StepArgs A;
+  A.n1 = S.n1;
+  A.n2 = S.n2;
+  A.nsub = nsub;
+  A.nov = S.nov;
+  A.gnx = S.gnx;
+  A.gny = S.gny;
+  A.wnx = wnx;
+  A.wny = wny;
+  A.nw = nw;
+  A.nring = Y.nring;
+  A.ih2 = 1.0 / (S.h * S.h);
+  A.sub = d_sub;
+  A.sa = d_sa;
+  A.sa_stride = sa_stride;
+  A.wx = d_wx;
+  A.wy = d_wy;
+  A.k2 = d_k2;
+  A.perm = d_perm;
+  A.pinv = d_pinv;
+  A.f = f;
+  A.fany = d_fany;
+  A.zc = d_Z[s % 3];
+  A.zp1 = d_Z[(s + 2) % 3];
+  A.zp2 = d_Z[(s + 1) % 3];
+  A.B = d_B;
+  A.Ucur = d_U[s % 3];
+  A.Up1 = d_U[(s + 2) % 3];
+  A.Up2 = d_U[(s + 1) % 3];
+  A.asmb = d_asm;
+  A.colcov = d_colcov;
+  A.rowcov = d_rowcov;
+  A.step = s;
+  A.cls_ptr = d_cls_ptr;
+  A.cls_mem = d_cls_mem;
+  A.act_ptr = d_act_ptr;
+  A.act_list = d_act_list;
+  A.counts = d_counts;
+  return A;
+}
+
+__global__ void k_fill_int(int* p, int v, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = v;
+}
+
+void hddm_engine::fill_flags(int* p, int v, int n) {
+  k_fill_int<<<(n + 255) / 256, 256, 0, st>>>(p, v, n);
+}
+
+// reset_state, ddm.cpp:152-157
+void hddm_engine::reset_state() {
+  for (int k = 0; k < 3; ++k) fill_flags(d_Z[k], 1, nsub);
+  CK(cudaMemsetAsync(d_asm, 0, ng * sizeof(cplx), st));
+  last_step = 0;
+}
+
+// one DDM iteration, DdmEngine::sweep (ddm.cpp:174-214)
+void hddm_engine::enqueue_step(int s, const cplx* f) {
+  const StepArgs A = step_args(s, f);
+  stage_begin(0);
+  launch_flags(A, ncls, st);
+  launch_gather(A, st);
+  stage_end(0);
+  stage_begin(1);
+  launch_solve(solve_args(d_B, A.Ucur, d_Y), plan, ncls, max_members, st);
+  stage_end(1);
+  stage_begin(2);
+  CheckArgs C;
+  C.nw = nw;
+  C.wnx = wnx;
+  C.wny = wny;
+  C.gnx = S.gnx;
+  C.nring = Y.nring;
+  C.ih2 = A.ih2;
+  C.sub = d_sub;
+  C.sa = d_sa;
+  C.sa_stride = sa_stride;
+  C.k2 = d_k2;
+  C.perm = d_perm;
+  C.pinv = d_pinv;
+  C.zc = A.zc;
+  C.nsub = nsub;
+  C.B = d_B;
+  C.X = A.Ucur;
+  C.part = d_part_chk;
+  C.nchunk = nchunk;
+  C.rel = d_rel;
+  C.refine_flag = d_refine;
+  C.max_rel = d_maxrel;
+  launch_check(C, st);
+  stage_end(2);
+  stage_begin(3);
+  launch_accumulate(A, st);
+  stage_end(3);
+  if (timing)
+    for (int k = 0; k < 4; ++k) stage_collect(k);
+  last_step = s;
+}
+
+double hddm_engine::device_norm(const cplx* v) {
+  launch_nrm2_part(v, ng, d_part, st);
+  launch_finish_sum(d_part, 1, d_scal, st);
+  CK(cudaMemcpyAsync(h_scal, d_scal, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return std::sqrt(h_scal[0]);
+}
+
+void hddm_engine::ensure_krylov(int m) {
+  if (kry_m >= m) return;
+  for (cplx* p : V) dfree(p);
+  for (cplx* p : Z) dfree(p);
+  V.clear();
+  Z.clear();
+  for (int i = 0; i <= m; ++i) V.push_back(dalloc<cplx>(ng));
+  for (int i = 0; i < m; ++i) Z.push_back(dalloc<cplx>(ng));
+  if (d_Zptr) dfree(d_Zptr);
+  d_Zptr = dalloc<cplx*>(m);
+  CK(cudaMemcpyAsync(d_Zptr, Z.data(), sizeof(cplx*) * m, cudaMemcpyHostToDevice, st));
+  for (cplx* p : {d_H, d_g, d_sn_g, d_y})
+    if (p) dfree(p);
+  if (d_cs) dfree(d_cs);
+  d_H = dalloc<cplx>(size_t(m) * (m + 1));
+  d_g = dalloc<cplx>(m + 1);
+  d_sn_g = dalloc<cplx>(m);
+  d_cs = dalloc<double>(m);
+  d_y = dalloc<cplx>(m);
+  if (!d_b) {
+    d_b = dalloc<cplx>(ng);
+    d_x = dalloc<cplx>(ng);
+    d_r = dalloc<cplx>(ng);
+  }
+  kry_m = m;
+}
+
+// ----------------------------------------------------------------- C-ABI
+namespace {
+
+template <class F>
+int guarded(hddm_engine* e, F&& fn) {
+  try {
+    if (e) CK(cudaSetDevice(e->dev));
+    fn();
+    return HDDM_OK;
+  } catch (const ConfigErr& x) {
+    (e ? e->err : g_err) = x.what();
+    return HDDM_ERR_CONFIG;
+  } catch (const SolveErr& x) {
+    (e ? e->err : g_err) = x.what();
+    return HDDM_ERR_SOLVE;
+  } catch (const std::exception& x) {
+    (e ? e->err : g_err) = x.what();
+    return HDDM_ERR_OTHER;
+  }
+}
+
+const cplx* in_ptr(hddm_engine* e, const double* p, int memkind, cplx* stage) {
+  if (memkind == HDDM_DEVICE) return reinterpret_cast<const cplx*>(p);
+  CK(cudaMemcpyAsync(stage, p, e->ng * sizeof(cplx), cudaMemcpyHostToDevice, e->st));
+  return stage;
+}
+
+void out_copy(hddm_engine* e, double* p, const cplx* src, int memkind) {
+  if (memkind == HDDM_DEVICE) {
+    if (reinterpret_cast<const cplx*>(p) != src)
+      CK(cudaMemcpyAsync(p, src, e->ng * sizeof(cplx), cudaMemcpyDeviceToDevice, e->st));
+  } else {
+    CK(cudaMemcpyAsync(p, src, e->ng * sizeof(cplx), cudaMemcpyDeviceToHost, e->st));
+  }
+}
+
+void read_counts(hddm_engine* e, long long* c) {
+  CK(cudaMemcpyAsync(c, e->d_counts, 2 * sizeof(long long), cudaMemcpyDeviceToHost, e->st));
+  CK(cudaStreamSynchronize(e->st));
+}
+
+void check_refine(hddm_engine* e) {
+  int flag = 0;
+  CK(cudaMemcpyAsync(&flag, e->d_refine, sizeof(int), cudaMemcpyDeviceToHost, e->st));
+  CK(cudaStreamSynchronize(e->st));
+  if (flag)
+    throw SolveErr(
+        "a local solve needed iterative-refinement corrections (relres > 1e-11); "
+        "correction passes are not implemented on the GPU path");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hddm_last_error(const hddm_engine* e) { return e ? e->err.c_str() : g_err.c_str(); }
+
+int hddm_create(const hddm_problem* p, hddm_engine** out) {
+  *out = nullptr;
+  auto e = std::make_unique<hddm_engine>();
+  const int rc = guarded(nullptr, [&] { e->create(*p); });
+  if (rc == HDDM_OK) *out = e.release();
+  return rc;
+}
+
+void hddm_destroy(hddm_engine* e) { delete e; }
+
+long hddm_n_global(const hddm_engine* e) { return long(e->ng); }
+double hddm_sigma0(const hddm_engine* e) { return e->S.sigma0; }
+double hddm_factor_ms(const hddm_engine* e) { return e->factor_ms; }
+int hddm_num_subdomains(const hddm_engine* e) { return e->nsub; }
+int hddm_num_classes(const hddm_engine* e) { return e->ncls; }
+int hddm_class_of(const hddm_engine* e, int t) {
+  return t >= 0 && t < e->nsub ? e->S.subs[t].cls : -1;
+}
+
+int hddm_class_info(const hddm_engine* e, int c, int* members, long* nnz, double* probe,
+                    int* is_ldlt) {
+  if (c < 0 || c >= e->ncls) return HDDM_ERR_CONFIG;
+  *members = e->S.cls_ptr[c + 1] - e->S.cls_ptr[c];
+  *nnz = long(e->Y.nnz_ref);
+  *probe = e->probe[c];
+  *is_ldlt = 1;
+  return HDDM_OK;
+}
+
+int hddm_window_dims(const hddm_engine* e, int* nx, int* ny) {
+  *nx = e->wnx;
+  *ny = e->wny;
+  return HDDM_OK;
+}
+
+int hddm_nd_order(int nx, int ny, int* order) {
+  const std::vector<int> o = nd_order(nx, ny);
+  std::copy(o.begin(), o.end(), order);
+  return HDDM_OK;
+}
+
+int hddm_footprint(const hddm_engine* e, long* stored, long* ref_nnz, long* device_bytes) {
+  *stored = long(e->Y.nvals);
+  *ref_nnz = long(e->Y.nnz_ref);
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  *device_bytes = long(total_b - free_b);
+  return HDDM_OK;
+}
+
+int hddm_apply_global(hddm_engine* e, const double* u, double* out, int memkind) {
+  return guarded(e, [&] {
+    const cplx* du = in_ptr(e, u, memkind, e->d_f);
+    GlobalArgs G{e->S.gnx, e->S.gny, 1.0 / (e->S.h * e->S.h), e->d_ga, e->d_k2};
+    cplx* dst = memkind == HDDM_DEVICE ? reinterpret_cast<cplx*>(out) : e->d_tmp;
+    launch_apply_global(G, du, dst, nullptr, nullptr, e->st);
+    if (memkind != HDDM_DEVICE) out_copy(e, out, dst, memkind);
+    CK(cudaStreamSynchronize(e->st));
+  });
+}
+
+int hddm_solve_iterative(hddm_engine* e, const double* f, double tol, int max_steps,
+                         int check_every, double* out, int memkind, hddm_stats* stats,
+                         int* hist_step, double* hist_rel, double* hist_ms, int hist_cap,
+                         int* hist_len) {
+  return guarded(e, [&] {
+    if (check_every < 1) check_every = 1;
+    hddm_stats st{};
+    st.relres = -1;
+    st.factor_ms = e->factor_ms;
+    const cplx* df = in_ptr(e, f, memkind, e->d_f);
+    const double bnorm = e->device_norm(df);
+    int nh = 0;
+    e->reset_state();
+    CK(cudaMemsetAsync(e->d_counts, 0, 2 * sizeof(long long), e->st));
+    CK(cudaMemsetAsync(e->d_refine, 0, sizeof(int), e->st));
+    if (bnorm == 0) {
+      st.converged = 1;
+      st.relres = 0;
+      CK(cudaMemsetAsync(e->d_asm, 0, e->ng * sizeof(cplx), e->st));
+    } else {
+      StepArgs A0 = e->step_args(1, df);
+      launch_fany(A0, e->st);
+      GlobalArgs G{e->S.gnx, e->S.gny, 1.0 / (e->S.h * e->S.h), e->d_ga, e->d_k2};
+      for (int s = 1; s <= max_steps; ++s) {
+        const double t0 = now_ms();
+        e->enqueue_step(s, df);
+        st.steps = s;
+        if (s % check_every == 0 || s == max_steps) {
+          // residual_norm, ddm.cpp:237-242
+          launch_apply_global(G, e->d_asm, nullptr, df, e->d_part, e->st);
+          launch_finish_sum(e->d_part, 1, e->d_scal, e->st);
+          CK(cudaMemcpyAsync(e->h_scal, e->d_scal, sizeof(double), cudaMemcpyDeviceToHost, e->st));
+          CK(cudaStreamSynchronize(e->st));
+          const double rel = std::sqrt(e->h_scal[0]) / bnorm;
+          const double ms = now_ms() - t0;
+          if (nh < hist_cap) {
+            if (hist_step) hist_step[nh] = s;
+            if (hist_rel) hist_rel[nh] = rel;
+            if (hist_ms) hist_ms[nh] = ms;
+          }
+          ++nh;
+          st.sweep_ms += ms;
+          st.relres = rel;
+          if (rel <= tol) {
+            st.converged = 1;
+            break;
+          }
+        } else {
+          st.sweep_ms += now_ms() - t0;
+        }
+      }
+    }
+    out_copy(e, out, e->d_asm, memkind);
+    long long cnt[2];
+    read_counts(e, cnt);
+    check_refine(e);
+    st.solves = long(cnt[0]);
+    st.skipped = long(cnt[1]);
+    if (hist_len) *hist_len = nh;
+    if (stats) *stats = st;
+  });
+}
+
+int hddm_precondition(hddm_engine* e, const double* r, double* z, int ksteps, int memkind,
+                      hddm_stats* stats) {
+  return guarded(e, [&] {
+    const cplx* dr = in_ptr(e, r, memkind, e->d_f);
+    const double t0 = now_ms();
+    e->reset_state();
+    CK(cudaMemsetAsync(e->d_counts, 0, 2 * sizeof(long long), e->st));
+    CK(cudaMemsetAsync(e->d_refine, 0, sizeof(int), e->st));
+    StepArgs A0 = e->step_args(1, dr);
+    launch_fany(A0, e->st);
+    for (int s = 1; s <= ksteps; ++s) e->enqueue_step(s, dr);
+    out_copy(e, z, e->d_asm, memkind);
+    long long cnt[2];
+    read_counts(e, cnt);
+    check_refine(e);
+    if (stats) {
+      stats->solves += long(cnt[0]);
+      stats->skipped += long(cnt[1]);
+      stats->sweep_ms += now_ms() - t0;
+      stats->factor_ms = e->factor_ms;
+    }
+  });
+}
+
+int hddm_fgmres(hddm_engine* e, const double* b, double* x, double tol, int max_iters,
+                int restart, int ksteps, int memkind, hddm_fgmres_result* res, double* hist,
+                int hist_cap, hddm_stats* pstats) {
+  return guarded(e, [&] {
+    const double tstart = now_ms();
+    hddm_fgmres_result R{};
+    R.relres = R.true_relres = -1;
+    const long long n = e->ng;
+    int mcap = restart > 0 ? restart : max_iters;
+    if (mcap < 1) mcap = 1;
+    e->ensure_krylov(mcap);
+    const int ld = mcap + 1;  // H column j: d_H[j*ld + i]
+    cudaStream_t st = e->st;
+    CK(cudaMemcpyAsync(e->d_b, b, n * sizeof(cplx),
+                       memkind == HDDM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(e->d_x, 0, n * sizeof(cplx), st));
+    CK(cudaMemsetAsync(e->d_refine, 0, sizeof(int), st));
+    const double bnorm = e->device_norm(e->d_b);
+    GlobalArgs G{e->S.gnx, e->S.gny, 1.0 / (e->S.h * e->S.h), e->d_ga, e->d_k2};
+    long long cnt_solves = 0, cnt_skipped = 0;
+    double sweep_ms = 0;
+    if (bnorm == 0) {
+      R.converged = 1;
+      R.relres = R.true_relres = 0;
+    } else {
+      CK(cudaMemcpyAsync(e->d_r, e->d_b, n * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+      int total = 0;
+      bool stop = false;
+      while (!stop && total < max_iters) {
+        const int m = restart > 0 ? std::min(restart, max_iters - total) : max_iters - total;
+        const double rnorm = e->device_norm(e->d_r);
+        if (rnorm == 0) {
+          R.converged = 1;
+          break;
+        }
+        e->h_scal[8] = rnorm;
+        CK(cudaMemcpyAsync(e->d_scal + 8, e->h_scal + 8, sizeof(double), cudaMemcpyHostToDevice, st));
+        launch_scale_div(e->V[0], e->d_r, e->d_scal + 8, n, st);
+        launch_init_g(e->d_g, m, e->d_scal + 8, st);
+        CK(cudaMemsetAsync(e->d_H, 0, sizeof(cplx) * size_t(mcap) * ld, st));
+        int k = 0;
+        for (int j = 0; j < m; ++j) {
+          const double it0 = now_ms();
+          // Z_j = M(V_j): K DDM sweeps (precondition, ddm.cpp:280-287)
+          e->reset_state();
+          CK(cudaMemsetAsync(e->d_counts, 0, 2 * sizeof(long long), st));
+          StepArgs A0 = e->step_args(1, e->V[j]);
+          launch_fany(A0, st);
+          const double ts = now_ms();
+          for (int s = 1; s <= ksteps; ++s) e->enqueue_step(s, e->V[j]);
+          CK(cudaMemcpyAsync(e->Z[j], e->d_asm, n * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+          // w = A Z_j
+          cplx* w = e->V[j + 1];
+          launch_apply_global(G, e->Z[j], w, nullptr, nullptr, st);
+          // MGS: h_0j, then fused (axpy_i, dot_{i+1} | norm)
+          cplx* Hc = e->d_H + size_t(j) * ld;
+          launch_dot_part(e->V[0], w, n, e->d_part, st);
+          launch_finish_sum(e->d_part, 2, reinterpret_cast<double*>(Hc), st);
+          for (int i = 0; i <= j; ++i) {
+            const cplx* Vn = i < j ? e->V[i + 1] : nullptr;
+            launch_axpy_dot(w, e->V[i], Hc + i, Vn, n, e->d_part, st);
+            if (Vn)
+              launch_finish_sum(e->d_part, 2, reinterpret_cast<double*>(Hc + i + 1), st);
+            else
+              launch_finish_sum(e->d_part, 1, e->d_scal + 4, st);  // |w|^2
+          }
+          launch_givens(Hc, e->d_scal + 4, e->d_cs, e->d_sn_g, e->d_g, j, bnorm, e->d_scal + 16,
+                        e->d_scal + 5, st);
+          CK(cudaMemcpyAsync(e->h_scal + 16, e->d_scal + 16, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+          long long cnt[2];
+          CK(cudaMemcpyAsync(cnt, e->d_counts, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st));
+          CK(cudaStreamSynchronize(st));
+          cnt_solves += cnt[0];
+          cnt_skipped += cnt[1];
+          sweep_ms += now_ms() - ts;
+          const int flags = int(e->h_scal[17]);
+          if (flags & 1) {  // dead column
+            stop = true;
+            break;
+          }
+          ++total;
+          k = j + 1;
+          R.relres = e->h_scal[16];
+          if (hist && total - 1 < hist_cap) hist[total - 1] = R.relres;
+          (void)it0;
+          if (R.relres <= tol) {
+            R.converged = 1;
+            stop = true;
+            break;
+          }
+          if (flags & 2) {  // hlast == 0
+            stop = true;
+            break;
+          }
+          launch_scale_div(w, w, e->d_scal + 5, n, st);
+        }
+        if (k > 0) {
+          launch_backsolve(e->d_H, ld, e->d_g, e->d_y, k, st);
+          launch_update_x(e->d_x, e->d_Zptr, e->d_y, k, n, st);
+        }
+        if (!stop) {
+          launch_apply_global(G, e->d_x, e->d_r, nullptr, nullptr, st);
+          launch_bsub(e->d_r, e->d_b, n, st);
+        }
+      }
+      R.iters = total;
+      // true residual, krylov.cpp:126-131
+      launch_apply_global(G, e->d_x, nullptr, e->d_b, e->d_part, st);
+      launch_finish_sum(e->d_part, 1, e->d_scal, st);
+      CK(cudaMemcpyAsync(e->h_scal, e->d_scal, sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      R.true_relres = std::sqrt(e->h_scal[0]) / bnorm;
+    }
+    out_copy(e, x, e->d_x, memkind);
+    CK(cudaStreamSynchronize(st));
+    check_refine(e);
+    R.wall_ms = now_ms() - tstart;
+    if (res) *res = R;
+    if (pstats) {
+      pstats->solves += long(cnt_solves);
+      pstats->skipped += long(cnt_skipped);
+      pstats->sweep_ms += sweep_ms;
+      pstats->factor_ms = e->factor_ms;
+    }
+  });
+}
+
+int hddm_tap_subdomain(hddm_engine* e, int t, double* rhs, double* u, int* active) {
+  return guarded(e, [&] {
+    if (t < 0 || t >= e->nsub || e->last_step < 1) throw ConfigErr("no sweep to tap");
+    const int s = e->last_step;
+    std::vector<cplx> b(e->nw), x(e->nw);
+    int z = 1;
+    CK(cudaMemcpyAsync(b.data(), e->d_B + size_t(t) * e->nw, e->nw * sizeof(cplx), cudaMemcpyDeviceToHost, e->st));
+    CK(cudaMemcpyAsync(x.data(), e->d_U[s % 3] + size_t(t) * e->nw, e->nw * sizeof(cplx), cudaMemcpyDeviceToHost, e->st));
+    CK(cudaMemcpyAsync(&z, e->d_Z[s % 3] + t, sizeof(int), cudaMemcpyDeviceToHost, e->st));
+    CK(cudaStreamSynchronize(e->st));
+    for (int k = 0; k < e->nw; ++k) {
+      const int node = e->Y.perm[k];
+      rhs[2 * node] = b[k].x;
+      rhs[2 * node + 1] = b[k].y;
+      u[2 * node] = x[k].x;
+      u[2 * node + 1] = x[k].y;
+    }
+    *active = z ? 0 : 1;
+  });
+}
+
+int hddm_class_solve(hddm_engine* e, int c, const double* b, double* x, double* relres) {
+  return guarded(e, [&] {
+    if (c < 0 || c >= e->ncls) throw ConfigErr("class index out of range");
+    const int t = e->S.cls_rep[c];
+    std::vector<cplx> bfo(e->nw);
+    for (int k = 0; k < e->nw; ++k) {
+      const int node = e->Y.perm[k];
+      bfo[k] = cmk(b[2 * node], b[2 * node + 1]);
+    }
+    std::vector<int> zc(e->nsub, 1), aptr(e->ncls + 1, 0), alist(1, t);
+    zc[t] = 0;
+    for (int k = c + 1; k <= e->ncls; ++k) aptr[k] = 1;
+    cudaStream_t st = e->st;
+    CK(cudaMemcpyAsync(e->d_B + size_t(t) * e->nw, bfo.data(), e->nw * sizeof(cplx), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(e->d_Z[0], zc.data(), sizeof(int) * e->nsub, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(e->d_act_ptr, aptr.data(), sizeof(int) * (e->ncls + 1), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(e->d_act_list, alist.data(), sizeof(int), cudaMemcpyHostToDevice, st));
+    launch_solve(e->solve_args(e->d_B, e->d_U[0], e->d_Y), e->plan, e->ncls, 1, st);
+    CheckArgs C;
+    C.nw = e->nw;
+    C.wnx = e->wnx;
+    C.wny = e->wny;
+    C.gnx = e->S.gnx;
+    C.nring = e->Y.nring;
+    C.ih2 = 1.0 / (e->S.h * e->S.h);
+    C.sub = e->d_sub;
+    C.sa = e->d_sa;
+    C.sa_stride = e->sa_stride;
+    C.k2 = e->d_k2;
+    C.perm = e->d_perm;
+    C.pinv = e->d_pinv;
+    C.zc = e->d_Z[0];
+    C.nsub = e->nsub;
+    C.B = e->d_B;
+    C.X = e->d_U[0];
+    C.part = e->d_part_chk;
+    C.nchunk = e->nchunk;
+    C.rel = e->d_rel;
+    C.refine_flag = e->d_refine;
+    C.max_rel = e->d_maxrel;
+    launch_check(C, st);
+    std::vector<cplx> xf(e->nw);
+    double rel = 0;
+    CK(cudaMemcpyAsync(xf.data(), e->d_U[0] + size_t(t) * e->nw, e->nw * sizeof(cplx), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&rel, e->d_rel + t, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int k = 0; k < e->nw; ++k) {
+      const int node = e->Y.perm[k];
+      x[2 * node] = xf[k].x;
+      x[2 * node + 1] = xf[k].y;
+    }
+    if (relres) *relres = rel;
+    e->last_step = 0;
+  });
+}
+
+int hddm_set_timing(hddm_engine* e, int enable) {
+  e->timing = enable != 0;
+  for (double& v : e->stage_ms) v = 0;
+  return HDDM_OK;
+}
+
+int hddm_stage_times(const hddm_engine* e, double* ms, int cap, int* n) {
+  for (int k = 0; k < kStages && k < cap; ++k) ms[k] = e->stage_ms[k];
+  *n = kStages;
+  return HDDM_OK;
+}
+
+const char* hddm_stage_name(int i) { return i >= 0 && i < kStages ? kStageNames[i] : ""; }
+
+void* hddm_stream(const hddm_engine* e) { return e->st; }
+
+}  // extern "C"

@@ -1,0 +1,144 @@
+// Kernel argument blocks and launcher prototypes (host <-> .cu glue).
+#pragma once
+
+#include <vector>
+
+#include "dev.cuh"
+
+namespace hddm {
+
+// ------------------------------------------------------------------ solves
+struct SolveArgs {
+  const DevSn* sn;
+  const DevBlk* blk;
+  const int* row_first;
+  const long long* row_off;
+  const int* rin_ptr;  // per factor-order position: incoming forward entries
+  const RowIn* rin;
+  const cplx* vals;    // ncls x nvals
+  long long nvals;
+  const int* act_ptr;  // CSR over classes of right-hand-side ids
+  const int* act_list;
+  const cplx* B;       // right-hand sides (factor order), stride nw
+  cplx* X;             // solutions (factor order), stride nw
+  cplx* Y;             // scratch, stride nw
+  int nw, nring;
+};
+
+struct SolveLevel {
+  int ntask = 0;
+  Task* d_tasks = nullptr;
+};
+
+struct SolvePlan {
+  int nleaf = 0;
+  int* d_leaves = nullptr;
+  std::vector<SolveLevel> fwd, bwd;
+};
+
+void launch_solve(const SolveArgs& A, const SolvePlan& P, int ncls, int max_members,
+                  cudaStream_t st);
+
+// ------------------------------------------------------------------ factor
+struct FactorArgs {
+  const DevSn* sn;
+  const DevBlk* blk;
+  const int* row_first;
+  const long long* row_off;
+  const int* extadd;
+  const int* aent_i;
+  const int* aent_j;
+  const cplx* aval;   // ncls x naent
+  int naent;
+  cplx* front;        // ncls x front_words
+  long long front_words;
+  cplx* vals;         // ncls x nvals
+  long long nvals;
+  int* status;        // per class: 0 ok, 1 zero pivot
+};
+
+void launch_factor_level(const FactorArgs& A, const int* d_nodes, int nnodes, int ncls,
+                         cudaStream_t st);
+
+// ------------------------------------------------------------------ DDM step
+struct StepArgs {
+  // geometry
+  int n1, n2, nsub, nov, gnx, gny, wnx, wny, nw, nring;
+  double ih2;
+  const DevSub* sub;
+  const cplx* sa;        // per-sub alpha arrays: a1n[wnx] ia1h[wnx] a2n[wny] ia2h[wny]
+  int sa_stride;
+  const double* wx;      // per-sub blend weights (nsub x wnx)
+  const double* wy;      // (nsub x wny)
+  const double* k2;      // global nodal k^2
+  const int* perm;       // window node -> ... (perm[pos] = node)
+  const int* pinv;       // node -> pos
+  // state
+  const cplx* f;         // global source/rhs of this sweep sequence
+  const int* fany;       // per-sub: owned f has a nonzero
+  int* zc;               // flags of this step (1 = zero/skipped)
+  const int* zp1;
+  const int* zp2;
+  cplx* B;               // rhs (factor order)
+  cplx* Ucur;            // this step's solutions (factor order)
+  const cplx* Up1;       // previous step
+  const cplx* Up2;       // two steps back
+  cplx* asmb;            // assembled global field
+  const int* colcov;     // per global column: up to 4 covering i (-1 pad)
+  const int* rowcov;     // per global row: up to 4 covering j
+  int step;
+  // class membership and active lists
+  const int* cls_ptr;
+  const int* cls_mem;
+  int* act_ptr;
+  int* act_list;
+  long long* counts;     // [0] solves, [1] skipped
+};
+
+void launch_fany(const StepArgs& A, cudaStream_t st);
+void launch_flags(const StepArgs& A, int ncls, cudaStream_t st);
+void launch_gather(const StepArgs& A, cudaStream_t st);
+void launch_accumulate(const StepArgs& A, cudaStream_t st);
+
+// per-RHS residual check of the local solve (refine's first pass,
+// proj/src/sparse.cpp:268-292): rel[t] = ||B - A X|| / ||B||
+struct CheckArgs {
+  int nw, wnx, wny, gnx, nring;
+  double ih2;
+  const DevSub* sub;
+  const cplx* sa;
+  int sa_stride;
+  const double* k2;
+  const int* perm;
+  const int* pinv;
+  const int* zc;      // per RHS: 1 = inactive
+  int nsub;
+  const cplx* B;
+  const cplx* X;
+  double* part;      // nsub x nchunk x 2
+  int nchunk;
+  double* rel;       // per sub
+  int* refine_flag;  // set when any rel > 1e-11
+  double* max_rel;
+};
+void launch_check(const CheckArgs& A, cudaStream_t st);
+
+// ------------------------------------------------------------------ global
+struct GlobalArgs {
+  int gnx, gny;
+  double ih2;
+  const cplx* ga;   // a1n[gnx] ia1h[gnx] a2n[gny] ia2h[gny]
+  const double* k2;
+};
+// out = L u (ring identity); if f != nullptr also partial sums of |f - out|^2
+void launch_apply_global(const GlobalArgs& G, const cplx* u, cplx* out, const cplx* f,
+                         double* part, cudaStream_t st);
+int reduce_blocks();  // number of partials the reduction kernels produce
+
+// deterministic reductions / BLAS-1 over n complex
+void launch_nrm2_part(const cplx* v, long long n, double* part, cudaStream_t st);
+void launch_dot_part(const cplx* a, const cplx* b, long long n, double* part, cudaStream_t st);
+// sum partials (reduce_blocks() of them, stride 1 or 2 doubles) into out
+void launch_finish_sum(const double* part, int ncomp, double* out, cudaStream_t st);
+
+}  // namespace hddm

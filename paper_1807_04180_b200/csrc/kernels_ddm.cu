@@ -1,0 +1,398 @@
+// DDM step kernels: zero-flag bookkeeping, the fused gather-sources kernel
+// (restrict_owned + 8-direction add_transfer + scale_rhs), the blend-accumulate,
+// the local-solve residual check, the global stencil and deterministic
+// reductions.
+//
+// Reference semantics reproduced (proj/src/ddm.cpp:174-242, transfer.cpp:7-88):
+//   * step 1 only sees f (restrict_owned on the owned rectangle);
+//   * edge transfers read step s-1, corner transfers read step s-2;
+//   * a subdomain is skipped iff it has no nonzero owned f (step 1) and every
+//     in-range source is zero-flagged; values of transferred sources are never
+//     inspected;
+//   * the assembled field adds w_x w_y u_t in ascending t at every node.
+#include "dev.cuh"
+#include "kernels.cuh"
+
+namespace hddm {
+
+namespace {
+
+constexpr int kRedBlocks = 592;  // 4 x 148 SMs: fixed grid => fixed summation order
+__constant__ int kDI[8] = {+1, -1, 0, 0, +1, -1, +1, -1};  // source offsets in
+__constant__ int kDJ[8] = {0, 0, +1, -1, +1, +1, -1, -1};  // kGatherOrder L,R,D,U,DL,DR,UL,UR
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  double r = 0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < int(blockDim.x >> 5); ++i) r += sh[i];
+  return r;  // valid in thread 0
+}
+
+}  // namespace
+
+int reduce_blocks() { return kRedBlocks; }
+
+// fany[t] = owned rectangle of f holds a nonzero (restrict_owned, ddm.cpp:159-172)
+__global__ void k_fany(StepArgs A) {
+  const int t = blockIdx.x;
+  const DevSub S = A.sub[t];
+  const int w = S.own1 - S.own0 + 1, h = S.own3 - S.own2 + 1;
+  int any = 0;
+  for (int k = threadIdx.x; k < w * h && !any; k += blockDim.x) {
+    const int P = S.own0 + k % w, Q = S.own2 + k / w;
+    const cplx v = A.f[(long long)Q * A.gnx + P];
+    any = (v.x != 0.0 || v.y != 0.0);
+  }
+  any = __syncthreads_or(any);
+  if (threadIdx.x == 0) const_cast<int*>(A.fany)[t] = any;
+}
+
+void launch_fany(const StepArgs& A, cudaStream_t st) {
+  k_fany<<<A.nsub, 256, 0, st>>>(A);
+}
+
+// zero flags, active lists per class, solve/skip counters (ddm.cpp:187-207)
+__global__ void k_flags(StepArgs A, int ncls) {
+  extern __shared__ int sh[];  // ncls counts
+  for (int t = threadIdx.x; t < A.nsub; t += blockDim.x) {
+    const DevSub S = A.sub[t];
+    int any = (A.step == 1) ? A.fany[t] : 0;
+    for (int d = 0; d < 8; ++d) {
+      const int si = S.i + kDI[d], sj = S.j + kDJ[d];
+      if (si < 0 || si >= A.n1 || sj < 0 || sj >= A.n2) continue;
+      const int src = sj * A.n1 + si;
+      if (!(d >= 4 ? A.zp2 : A.zp1)[src]) any = 1;
+    }
+    A.zc[t] = any ? 0 : 1;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < ncls; c += blockDim.x) {
+    int cnt = 0;
+    for (int k = A.cls_ptr[c]; k < A.cls_ptr[c + 1]; ++k) cnt += A.zc[A.cls_mem[k]] ? 0 : 1;
+    sh[c] = cnt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int c = 0; c < ncls; ++c) {
+      A.act_ptr[c] = acc;
+      acc += sh[c];
+    }
+    A.act_ptr[ncls] = acc;
+    A.counts[0] += acc;
+    A.counts[1] += A.nsub - acc;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < ncls; c += blockDim.x) {
+    int o = A.act_ptr[c];
+    for (int k = A.cls_ptr[c]; k < A.cls_ptr[c + 1]; ++k)
+      if (!A.zc[A.cls_mem[k]]) A.act_list[o++] = A.cls_mem[k];
+  }
+}
+
+void launch_flags(const StepArgs& A, int ncls, cudaStream_t st) {
+  k_flags<<<1, 256, sizeof(int) * ncls, st>>>(A, ncls);
+}
+
+// ------------------------------------------------------------ gather sources
+namespace {
+
+// transfer_beta (partition.cpp:131-152)
+__device__ __forceinline__ double tbeta(int d, const DevSub& T, int nov, int p, int q) {
+  const bool fromL = d == 1 || d == 5 || d == 7;  // Right, DownRight, UpRight
+  const bool fromR = d == 0 || d == 4 || d == 6;  // Left, DownLeft, UpLeft
+  const bool fromB = d == 3 || d == 6 || d == 7;  // Up, UpLeft, UpRight
+  const bool fromT = d == 2 || d == 4 || d == 5;  // Down, DownLeft, DownRight
+  double b = 1.0;
+  if (fromL) b = beta0(double(p - T.cx0 - 1) / nov);
+  if (fromR) b = beta0(double(T.cx1 - 1 - p) / nov);
+  double c = 1.0;
+  if (fromB) c = beta0(double(q - T.cy0 - 1) / nov);
+  if (fromT) c = beta0(double(T.cy1 - 1 - q) / nov);
+  if ((fromL || fromR) && (fromB || fromT)) return b * c;
+  return (fromL || fromR) ? b : c;
+}
+
+// transfer_patch (transfer.cpp:7-62): is global node (P,Q) in direction d's patch
+__device__ __forceinline__ bool in_patch(int d, const DevSub& T, int wnx, int wny, int nov,
+                                         int P, int Q) {
+  int p0 = T.wx0 + 1, p1 = T.wx0 + wnx - 2, q0 = T.wy0 + 1, q1 = T.wy0 + wny - 2;
+  const bool fromL = d == 1 || d == 5 || d == 7;
+  const bool fromR = d == 0 || d == 4 || d == 6;
+  const bool fromB = d == 3 || d == 6 || d == 7;
+  const bool fromT = d == 2 || d == 4 || d == 5;
+  if (fromL) { p0 = max(p0, T.cx0 + 1); p1 = min(p1, T.cx0 + 1 + nov); }
+  if (fromR) { p0 = max(p0, T.cx1 - 1 - nov); p1 = min(p1, T.cx1 - 1); }
+  if (fromB) { q0 = max(q0, T.cy0 + 1); q1 = min(q1, T.cy0 + 1 + nov); }
+  if (fromT) { q0 = max(q0, T.cy1 - 1 - nov); q1 = min(q1, T.cy1 - 1); }
+  return P >= p0 && P <= p1 && Q >= q0 && Q <= q1;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(256) k_gather(StepArgs A) {
+  const int t = blockIdx.y;
+  if (A.zc[t]) return;
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= A.nw) return;
+  cplx* Bt = A.B + (long long)t * A.nw;
+  const int node = A.perm[pos];
+  const int lp = node % A.wnx, lq = node / A.wnx;
+  if (lp == 0 || lq == 0 || lp == A.wnx - 1 || lq == A.wny - 1) {
+    Bt[pos] = cmk(0, 0);
+    return;
+  }
+  const DevSub T = A.sub[t];
+  const int P = T.wx0 + lp, Q = T.wy0 + lq;
+  const cplx* sa = A.sa + (long long)t * A.sa_stride;
+  const cplx* a1n = sa;
+  const cplx* ia1h = sa + A.wnx;
+  const cplx* a2n = sa + 2 * A.wnx;
+  const cplx* ia2h = sa + 2 * A.wnx + A.wny;
+  const cplx jac = cmul(a1n[lp], a2n[lq]);
+  cplx val = cmk(0, 0);
+  if (A.step == 1 && P >= T.own0 && P <= T.own1 && Q >= T.own2 && Q <= T.own3)
+    val = A.f[(long long)Q * A.gnx + P];
+  const double k2 = A.k2[(long long)Q * A.gnx + P];
+  for (int d = 0; d < 8; ++d) {
+    const int si = T.i + kDI[d], sj = T.j + kDJ[d];
+    if (si < 0 || si >= A.n1 || sj < 0 || sj >= A.n2) continue;
+    const int src = sj * A.n1 + si;
+    const bool corner = d >= 4;
+    if ((corner ? A.zp2 : A.zp1)[src]) continue;
+    if (!in_patch(d, T, A.wnx, A.wny, A.nov, P, Q)) continue;
+    const DevSub S = A.sub[src];
+    const cplx* V = (corner ? A.Up2 : A.Up1) + (long long)src * A.nw;
+    // w = beta_d * v_src (zero outside the source window) at the 5 stencil nodes
+    auto w = [&](int p, int q) -> cplx {
+      const int sp = p - S.wx0, sq = q - S.wy0;
+      if (sp < 0 || sq < 0 || sp >= A.wnx || sq >= A.wny) return cmk(0, 0);
+      const cplx v = V[A.pinv[sq * A.wnx + sp]];
+      if (v.x == 0.0 && v.y == 0.0) return cmk(0, 0);
+      return cscale(v, tbeta(d, T, A.nov, p, q));
+    };
+    const cplx uc = w(P, Q);
+    const cplx ex = cscale(a2n[lq], A.ih2);
+    const cplx ey = cscale(a1n[lp], A.ih2);
+    // DiscreteOperator::stencil (discretize.hpp:43-54), same operation order
+    cplx tt = cmul(cmul(ex, ia1h[lp]), csub(w(P + 1, Q), uc));
+    tt = csub(tt, cmul(cmul(ex, ia1h[lp - 1]), csub(uc, w(P - 1, Q))));
+    tt = cadd(tt, cmul(cmul(ey, ia2h[lq]), csub(w(P, Q + 1), uc)));
+    tt = csub(tt, cmul(cmul(ey, ia2h[lq - 1]), csub(uc, w(P, Q - 1))));
+    const cplx Lw = cadd(cdiv(tt, jac), cscale(uc, k2));
+    val = csub(val, Lw);
+  }
+  Bt[pos] = cmul(jac, val);  // scale_rhs (discretize.cpp:162-172)
+}
+
+void launch_gather(const StepArgs& A, cudaStream_t st) {
+  dim3 g((A.nw + 255) / 256, A.nsub);
+  k_gather<<<g, 256, 0, st>>>(A);
+}
+
+// ------------------------------------------------------------ accumulate
+__global__ void __launch_bounds__(256) k_accumulate(StepArgs A) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)A.gnx * A.gny) return;
+  const int P = int(idx % A.gnx), Q = int(idx / A.gnx);
+  cplx acc = A.asmb[idx];
+  bool touched = false;
+  for (int b = 0; b < 4; ++b) {
+    const int j = A.rowcov[4 * Q + b];
+    if (j < 0) break;
+    for (int a = 0; a < 4; ++a) {
+      const int i = A.colcov[4 * P + a];
+      if (i < 0) break;
+      const int t = j * A.n1 + i;
+      if (A.zc[t]) continue;
+      const DevSub T = A.sub[t];
+      const double wy = A.wy[(long long)t * A.wny + (Q - T.wy0)];
+      if (wy == 0.0) continue;
+      const double w = A.wx[(long long)t * A.wnx + (P - T.wx0)] * wy;
+      if (w == 0.0) continue;
+      const cplx u = A.Ucur[(long long)t * A.nw + A.pinv[(Q - T.wy0) * A.wnx + (P - T.wx0)]];
+      acc.x = __dadd_rn(acc.x, __dmul_rn(w, u.x));
+      acc.y = __dadd_rn(acc.y, __dmul_rn(w, u.y));
+      touched = true;
+    }
+  }
+  if (touched) A.asmb[idx] = acc;
+}
+
+void launch_accumulate(const StepArgs& A, cudaStream_t st) {
+  const long long n = (long long)A.gnx * A.gny;
+  k_accumulate<<<unsigned((n + 255) / 256), 256, 0, st>>>(A);
+}
+
+// ------------------------------------------------------------ residual check
+__global__ void __launch_bounds__(256) k_check(CheckArgs A) {
+  __shared__ double sh[32];
+  const int t = blockIdx.y;
+  const bool act = !A.zc[t];
+  double r2 = 0, b2 = 0;
+  if (act) {
+    const cplx* X = A.X + (long long)t * A.nw;
+    const cplx* Bv = A.B + (long long)t * A.nw;
+    const DevSub T = A.sub[t];
+    const cplx* sa = A.sa + (long long)t * A.sa_stride;
+    const cplx* a1n = sa;
+    const cplx* ia1h = sa + A.wnx;
+    const cplx* a2n = sa + 2 * A.wnx;
+    const cplx* ia2h = sa + 2 * A.wnx + A.wny;
+    const int chunk = (A.nw + A.nchunk - 1) / A.nchunk;
+    const int p0 = blockIdx.x * chunk, p1 = min(A.nw, p0 + chunk);
+    for (int pos = p0 + threadIdx.x; pos < p1; pos += blockDim.x) {
+      const cplx b = Bv[pos];
+      b2 += cnorm2(b);
+      const int node = A.perm[pos];
+      const int lp = node % A.wnx, lq = node / A.wnx;
+      cplx ax;
+      if (lp == 0 || lq == 0 || lp == A.wnx - 1 || lq == A.wny - 1) {
+        ax = X[pos];
+      } else {
+        // J-scaled row of the assembled matrix (discretize.cpp:131-158)
+        const cplx ew = cscale(cmul(a2n[lq], ia1h[lp - 1]), A.ih2);
+        const cplx ee = cscale(cmul(a2n[lq], ia1h[lp]), A.ih2);
+        const cplx es = cscale(cmul(a1n[lp], ia2h[lq - 1]), A.ih2);
+        const cplx en = cscale(cmul(a1n[lp], ia2h[lq]), A.ih2);
+        const double k2 = A.k2[(long long)(T.wy0 + lq) * A.gnx + T.wx0 + lp];
+        const cplx diag = cadd(cmk(-(ew.x + ee.x + es.x + en.x), -(ew.y + ee.y + es.y + en.y)),
+                               cscale(cmul(a1n[lp], a2n[lq]), k2));
+        ax = cmul(diag, X[pos]);
+        if (lq > 1) cfma(ax, es, X[A.pinv[node - A.wnx]]);
+        if (lp > 1) cfma(ax, ew, X[A.pinv[node - 1]]);
+        if (lp < A.wnx - 2) cfma(ax, ee, X[A.pinv[node + 1]]);
+        if (lq < A.wny - 2) cfma(ax, en, X[A.pinv[node + A.wnx]]);
+      }
+      r2 += cnorm2(csub(b, ax));
+    }
+  }
+  const double R = block_sum(r2, sh);
+  const double Bs = block_sum(b2, sh);
+  if (threadIdx.x == 0) {
+    A.part[((long long)t * A.nchunk + blockIdx.x) * 2 + 0] = R;
+    A.part[((long long)t * A.nchunk + blockIdx.x) * 2 + 1] = Bs;
+  }
+}
+
+__global__ void k_check_finish(CheckArgs A, int nsub) {
+  for (int t = threadIdx.x; t < nsub; t += blockDim.x) {
+    double r2 = 0, b2 = 0;
+    for (int k = 0; k < A.nchunk; ++k) {
+      r2 += A.part[((long long)t * A.nchunk + k) * 2];
+      b2 += A.part[((long long)t * A.nchunk + k) * 2 + 1];
+    }
+    const double rel = b2 > 0 ? sqrt(r2) / sqrt(b2) : 0.0;
+    A.rel[t] = rel;
+    if (rel > 1e-11) atomicOr(A.refine_flag, 1);
+    // max_rel: deterministic (max is order-free); atomicMax on the bit pattern of a
+    // nonnegative double preserves ordering
+    atomicMax(reinterpret_cast<unsigned long long*>(A.max_rel),
+              (unsigned long long)__double_as_longlong(rel));
+  }
+}
+
+void launch_check(const CheckArgs& A, cudaStream_t st) {
+  dim3 g(A.nchunk, A.nsub);
+  k_check<<<g, 256, 0, st>>>(A);
+  k_check_finish<<<1, 256, 0, st>>>(A, A.nsub);
+}
+
+// ------------------------------------------------------------ global stencil
+// DiscreteOperator::apply (discretize.cpp:81-96) on the global window; when f is
+// given, also per-block partial sums of |f - L u|^2 (residual_norm, ddm.cpp:237-242).
+__global__ void __launch_bounds__(256) k_apply_global(GlobalArgs G, const cplx* u, cplx* out,
+                                                      const cplx* f, double* part) {
+  __shared__ double sh[32];
+  const long long n = (long long)G.gnx * G.gny;
+  const cplx* a1n = G.ga;
+  const cplx* ia1h = G.ga + G.gnx;
+  const cplx* a2n = G.ga + 2 * G.gnx;
+  const cplx* ia2h = G.ga + 2 * G.gnx + G.gny;
+  double acc = 0;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int p = int(idx % G.gnx), q = int(idx / G.gnx);
+    cplx o;
+    if (p == 0 || q == 0 || p == G.gnx - 1 || q == G.gny - 1) {
+      o = u[idx];
+    } else {
+      const cplx uc = u[idx];
+      const cplx ex = cscale(a2n[q], G.ih2);
+      const cplx ey = cscale(a1n[p], G.ih2);
+      cplx tt = cmul(cmul(ex, ia1h[p]), csub(u[idx + 1], uc));
+      tt = csub(tt, cmul(cmul(ex, ia1h[p - 1]), csub(uc, u[idx - 1])));
+      tt = cadd(tt, cmul(cmul(ey, ia2h[q]), csub(u[idx + G.gnx], uc)));
+      tt = csub(tt, cmul(cmul(ey, ia2h[q - 1]), csub(uc, u[idx - G.gnx])));
+      o = cadd(cdiv(tt, cmul(a1n[p], a2n[q])), cscale(uc, G.k2[idx]));
+    }
+    if (out) out[idx] = o;
+    if (f) acc += cnorm2(csub(f[idx], o));
+  }
+  if (part) {
+    const double s = block_sum(acc, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+  }
+}
+
+void launch_apply_global(const GlobalArgs& G, const cplx* u, cplx* out, const cplx* f,
+                         double* part, cudaStream_t st) {
+  k_apply_global<<<kRedBlocks, 256, 0, st>>>(G, u, out, f, part);
+}
+
+// ------------------------------------------------------------ reductions
+__global__ void __launch_bounds__(256) k_nrm2_part(const cplx* v, long long n, double* part) {
+  __shared__ double sh[32];
+  double acc = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    acc += cnorm2(v[i]);
+  const double s = block_sum(acc, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(256) k_dot_part(const cplx* a, const cplx* b, long long n,
+                                                  double* part) {
+  __shared__ double sh[32];
+  double re = 0, im = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const cplx x = a[i], y = b[i];  // conj(x) * y
+    re += x.x * y.x + x.y * y.y;
+    im += x.x * y.y - x.y * y.x;
+  }
+  const double s0 = block_sum(re, sh);
+  const double s1 = block_sum(im, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = s0;
+    part[2 * blockIdx.x + 1] = s1;
+  }
+}
+
+// one warp sums the partials in a fixed order
+__global__ void k_finish_sum(const double* part, int ncomp, double* out) {
+  const int lane = threadIdx.x;
+  for (int c = 0; c < ncomp; ++c) {
+    double acc = 0;
+    for (int i = lane; i < kRedBlocks; i += 32) acc += part[i * ncomp + c];
+    acc = warp_sum(acc);
+    if (lane == 0) out[c] = acc;
+  }
+}
+
+void launch_nrm2_part(const cplx* v, long long n, double* part, cudaStream_t st) {
+  k_nrm2_part<<<kRedBlocks, 256, 0, st>>>(v, n, part);
+}
+void launch_dot_part(const cplx* a, const cplx* b, long long n, double* part, cudaStream_t st) {
+  k_dot_part<<<kRedBlocks, 256, 0, st>>>(a, b, n, part);
+}
+void launch_finish_sum(const double* part, int ncomp, double* out, cudaStream_t st) {
+  k_finish_sum<<<1, 32, 0, st>>>(part, ncomp, out);
+}
+
+}  // namespace hddm
