@@ -148,12 +148,15 @@ int hddm_nd_order(int nx, int ny, int* order);
  * reference's nnz(L)+n per class, total device bytes held by the engine. */
 int hddm_footprint(const hddm_engine* e, long* stored_per_class,
                    long* ref_nnz_per_class, long* device_bytes);
-/* Run K DDM steps of the preconditioner on device vectors without
- * synchronising (bench helper); per-kernel-kind device times (ms) of the last
- * call can be read with hddm_stage_times when timing was enabled. */
+/* Per-stage device timing (CUDA events on the engine stream, resolved
+ * lazily, so the timed region is not synchronised): enable/reset, then read
+ * the accumulated milliseconds and event-pair counts per stage
+ * (hddm_stage_name(i)). hddm_launch_count: kernels this engine launched since
+ * the last hddm_set_timing. */
 int hddm_set_timing(hddm_engine* e, int enable);
-int hddm_stage_times(const hddm_engine* e, double* ms, int cap, int* n);
+int hddm_stage_times(hddm_engine* e, double* ms, long long* count, int cap, int* n);
 const char* hddm_stage_name(int i);
+long long hddm_launch_count(const hddm_engine* e);
 /* CUDA stream (cudaStream_t) the engine orders its work on. */
 void* hddm_stream(const hddm_engine* e);
 

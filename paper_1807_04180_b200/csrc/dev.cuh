@@ -62,9 +62,11 @@ struct Task {
   int s, a, b, pad;
 };
 
-// incoming forward entry for one separator row: profile row of a descendant
-struct RowIn {
-  int rowtab, src_c0, src_n, pad;
+// backward row of a supernode's block: value offset of the row's first stored
+// column, that column, and the destination (ancestor) position
+struct BwRow {
+  long long off;
+  int first, dpos;
 };
 
 struct DevSub {

@@ -73,7 +73,6 @@ struct hddm_engine {
   std::vector<void*> allocs;
   int last_step = 0;
   bool timing = false;
-  cudaEvent_t ev[2 * kStages] = {};
   double stage_ms[kStages] = {};
 
   // symbolic tables
@@ -81,8 +80,11 @@ struct hddm_engine {
   DevBlk* d_blk = nullptr;
   int* d_row_first = nullptr;
   long long* d_row_off = nullptr;
-  int* d_rin_ptr = nullptr;
-  RowIn* d_rin = nullptr;
+  long long* d_run_off = nullptr;
+  int* d_seg_ptr = nullptr;
+  int2* d_seg = nullptr;
+  int* d_bw_ptr = nullptr;
+  BwRow* d_bw = nullptr;
   int* d_perm = nullptr;
   int* d_pinv = nullptr;
   SolvePlan plan;
@@ -156,8 +158,7 @@ struct hddm_engine {
   ~hddm_engine() {
     if (dev >= 0) cudaSetDevice(dev);
     for (void* p : allocs) cudaFree(p);
-    for (auto& e : ev)
-      if (e) cudaEventDestroy(e);
+    for (auto& e : ev_pool) cudaEventDestroy(e);
     if (h_scal) cudaFreeHost(h_scal);
     if (st) cudaStreamDestroy(st);
   }
@@ -171,20 +172,49 @@ struct hddm_engine {
   void reset_state();
   void fill_flags(int* p, int v, int n);
   double device_norm(const cplx* v);
+  // stage timing: events recorded on the engine stream, resolved lazily (no
+  // host synchronisation inside the timed region)
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<int, int>>> ev_marks;  // stage, (begin, end) pool idx
+  size_t ev_next = 0;
+  int open_ev[kStages] = {};
+  long long launches = 0;
+  cudaEvent_t next_event() {
+    if (ev_next == ev_pool.size()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_next++];
+  }
   void stage_begin(int k) {
-    if (timing) CK(cudaEventRecord(ev[2 * k], st));
+    if (!timing) return;
+    open_ev[k] = int(ev_next);
+    CK(cudaEventRecord(next_event(), st));
   }
   void stage_end(int k) {
-    if (timing) CK(cudaEventRecord(ev[2 * k + 1], st));
-  }
-  void stage_collect(int k) {
     if (!timing) return;
-    float ms = 0;
-    CK(cudaEventSynchronize(ev[2 * k + 1]));
-    CK(cudaEventElapsedTime(&ms, ev[2 * k], ev[2 * k + 1]));
-    stage_ms[k] += ms;
+    const int b = open_ev[k];
+    const int e = int(ev_next);
+    CK(cudaEventRecord(next_event(), st));
+    ev_marks.push_back({k, {b, e}});
   }
+  void stage_resolve() {
+    if (ev_marks.empty()) return;
+    CK(cudaStreamSynchronize(st));
+    for (auto& m : ev_marks) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, ev_pool[m.second.first], ev_pool[m.second.second]));
+      stage_ms[m.first] += ms;
+      stage_n[m.first] += 1;
+    }
+    ev_marks.clear();
+    ev_next = 0;
+  }
+  long long stage_n[kStages] = {};
   void ensure_krylov(int m);
+  void build_plan();
+  int solve_launches() const { return solve_launch_count(plan); }
 };
 
 // ----------------------------------------------------------------- creation
@@ -196,7 +226,6 @@ void hddm_engine::create(const hddm_problem& p) {
   if (dev < 0 || dev >= ndev) throw ConfigErr("invalid CUDA device ordinal");
   CK(cudaSetDevice(dev));
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  for (auto& e : ev) CK(cudaEventCreate(&e));
   CK(cudaMallocHost(&h_scal, 64 * sizeof(double)));
   std::string msg;
   const int rc = build_setup(p, S, msg);
@@ -246,59 +275,36 @@ void hddm_engine::create(const hddm_problem& p) {
   d_row_off = upload(roff);
   d_perm = upload(Y.perm);
   d_pinv = upload(Y.pinv);
-  // incoming forward entries per separator row (fixed order: block index)
+  // forward runs and segments; backward rows per supernode
   {
-    std::vector<std::vector<RowIn>> per(nw);
-    for (size_t b = 0; b < Y.blk.size(); ++b) {
-      const Block& B = Y.blk[b];
-      const SnNode& src = Y.sn[B.src];
-      for (int r = 0; r < B.nr; ++r) {
-        const int rt = B.row0 + r;
-        if (Y.row_first[rt] >= src.n) continue;
-        per[Y.sn[B.dst].c0 + B.r0 + r].push_back({rt, src.c0, src.n, 0});
+    std::vector<long long> ro(Y.run_off.begin(), Y.run_off.end());
+    d_run_off = upload(ro);
+    d_seg_ptr = upload(Y.seg_ptr);
+    std::vector<int2> sg(Y.seg.size());
+    for (size_t k = 0; k < Y.seg.size(); ++k) sg[k] = make_int2(Y.seg[k].len, Y.seg[k].zbase);
+    d_seg = upload(sg);
+    std::vector<int> bptr(Y.sn.size() + 1, 0);
+    std::vector<BwRow> bw;
+    for (size_t s = 0; s < Y.sn.size(); ++s) {
+      bptr[s] = int(bw.size());
+      for (int b = Y.sn[s].blk0; b < Y.sn[s].blk0 + Y.sn[s].nblk; ++b) {
+        const Block& B = Y.blk[b];
+        for (int r = 0; r < B.nr; ++r) {
+          const int rt = B.row0 + r;
+          if (Y.row_first[rt] >= Y.sn[s].n) continue;  // empty padding row
+          BwRow w;
+          w.off = Y.row_off[rt];
+          w.first = Y.row_first[rt];
+          w.dpos = Y.sn[B.dst].c0 + B.r0 + r;
+          bw.push_back(w);
+        }
       }
     }
-    std::vector<int> ptr(nw + 1, 0);
-    std::vector<RowIn> all;
-    for (int k = 0; k < nw; ++k) {
-      ptr[k] = int(all.size());
-      all.insert(all.end(), per[k].begin(), per[k].end());
-    }
-    ptr[nw] = int(all.size());
-    d_rin_ptr = upload(ptr);
-    d_rin = upload(all);
+    bptr[Y.sn.size()] = int(bw.size());
+    d_bw_ptr = upload(bptr);
+    d_bw = upload(bw);
   }
-  // solve plan: leaves; forward levels by height; backward levels by depth
-  {
-    std::vector<int> leaves;
-    for (size_t s = 0; s < Y.sn.size(); ++s)
-      if (Y.sn[s].kind == 0) leaves.push_back(int(s));
-    plan.nleaf = int(leaves.size());
-    plan.d_leaves = upload(leaves);
-    const int R = 8, C = 256;
-    for (int h = 1; h <= Y.max_height; ++h) {
-      std::vector<Task> t;
-      for (size_t s = 0; s < Y.sn.size(); ++s)
-        if (Y.sn[s].kind == 1 && Y.sn[s].height == h)
-          for (int a = 0; a < Y.sn[s].n; a += R) t.push_back({int(s), a, std::min(a + R, Y.sn[s].n), 0});
-      if (t.empty()) continue;
-      SolveLevel L;
-      L.ntask = int(t.size());
-      L.d_tasks = upload(t);
-      plan.fwd.push_back(L);
-    }
-    for (int d = 0; d <= Y.max_depth; ++d) {
-      std::vector<Task> t;
-      for (size_t s = 0; s < Y.sn.size(); ++s)
-        if (Y.sn[s].kind == 1 && Y.sn[s].depth == d)
-          for (int a = 0; a < Y.sn[s].n; a += C) t.push_back({int(s), a, std::min(a + C, Y.sn[s].n), 0});
-      if (t.empty()) continue;
-      SolveLevel L;
-      L.ntask = int(t.size());
-      L.d_tasks = upload(t);
-      plan.bwd.push_back(L);
-    }
-  }
+  build_plan();
 
   // ---- per-subdomain data
   std::vector<DevSub> subs(nsub);
@@ -410,6 +416,121 @@ void hddm_engine::create(const hddm_problem& p) {
   run_probe();
 }
 
+// Solve plan: maximal subtrees of at most kSubtreeMax nodes run as one CTA each
+// (vectors in shared memory); the separators above them run level by level.
+void hddm_engine::build_plan() {
+  constexpr int kSubtreeMax = 600;
+  const int nsn = int(Y.sn.size());
+  std::vector<int> size(nsn, 0), cnt(nsn, 0);
+  for (int s = 0; s < nsn; ++s) {  // postorder: children first
+    size[s] = Y.sn[s].n;
+    cnt[s] = 1;
+    for (int k = 0; k < Y.sn[s].nch; ++k) {
+      size[s] += size[Y.sn[s].child[k]];
+      cnt[s] += cnt[Y.sn[s].child[k]];
+    }
+  }
+  std::vector<int> root_of(nsn, -1);
+  std::vector<int> roots;
+  for (int s = nsn - 1; s >= 0; --s) {  // parents before children
+    const int p = Y.sn[s].parent;
+    if (p >= 0 && root_of[p] >= 0) {
+      root_of[s] = root_of[p];
+    } else if (size[s] <= kSubtreeMax) {
+      root_of[s] = s;
+      roots.push_back(s);
+    }
+  }
+  std::sort(roots.begin(), roots.end());
+  std::vector<SubtreeInfo> st;
+  std::vector<Phase> ph;
+  std::vector<int2> items;
+  int np_max = 1, items_max = 1;
+  for (int r : roots) {
+    SubtreeInfo I;
+    I.np = size[r];
+    I.p0 = Y.sn[r].c0 + Y.sn[r].n - size[r];
+    I.ph0 = int(ph.size());
+    const int hmax = Y.sn[r].height;
+    for (int h = 0; h <= hmax; ++h) {
+      Phase P{};
+      P.kind = h == 0 ? 0 : 1;
+      P.it0 = int(items.size());
+      for (int s = r - cnt[r] + 1; s <= r; ++s) {
+        // supernodes of the subtree are a contiguous postorder index range
+        if (root_of[s] != r || Y.sn[s].height != h) continue;
+        if (h == 0)
+          items.push_back(make_int2(s, 0));
+        else
+          for (int i = 0; i < Y.sn[s].n; ++i) items.push_back(make_int2(s, i));
+      }
+      P.nit = int(items.size()) - P.it0;
+      if (P.nit == 0) continue;
+      items_max = std::max(items_max, P.nit);
+      if (h == 0) {  // leaf columns for the backward block products
+        P.ic0 = int(items.size());
+        for (int q = P.it0; q < P.it0 + P.nit; ++q)
+          for (int j = 0; j < Y.sn[items[q].x].n; ++j) items.push_back(make_int2(items[q].x, j));
+        P.nic = int(items.size()) - P.ic0;
+      }
+      ph.push_back(P);
+    }
+    I.nph = int(ph.size()) - I.ph0;
+    np_max = std::max(np_max, I.np);
+    st.push_back(I);
+  }
+  // sanity: a subtree's supernodes are the postorder index range [r-cnt+1, r]
+  for (int r : roots)
+    for (int s = r - cnt[r] + 1; s <= r; ++s)
+      if (root_of[s] != r) throw std::runtime_error("subtree is not contiguous in postorder");
+  plan.nsubtree = int(st.size());
+  plan.d_wprefix = dalloc<int>(ncls + 1);
+  plan.sub.st = upload(st);
+  plan.sub.ph = upload(ph);
+  plan.sub.items = upload(items);
+  plan.sub.np_max = np_max;
+  plan.sub.items_max = items_max;
+  // top separators: forward by height, backward by depth
+  const int R = 8, C = 256;
+  for (int h = 1; h <= Y.max_height; ++h) {
+    std::vector<Task> t;
+    for (int s = 0; s < nsn; ++s)
+      if (root_of[s] < 0 && Y.sn[s].height == h)
+        for (int a = 0; a < Y.sn[s].n; a += R) t.push_back({s, a, std::min(a + R, Y.sn[s].n), 0});
+    if (t.empty()) continue;
+    SolveLevel L;
+    L.ntask = int(t.size());
+    L.d_tasks = upload(t);
+    plan.fwd.push_back(L);
+  }
+  for (int d = 0; d <= Y.max_depth; ++d) {
+    std::vector<Task> t, t32;
+    for (int s = 0; s < nsn; ++s)
+      if (root_of[s] < 0 && Y.sn[s].depth == d) {
+        if (Y.sn[s].kind == 0) throw std::runtime_error("leaf above the subtree cut");
+        for (int a = 0; a < Y.sn[s].n; a += C) t.push_back({s, a, std::min(a + C, Y.sn[s].n), 0});
+        for (int a = 0; a < Y.sn[s].n; a += 32) t32.push_back({s, a, std::min(a + 32, Y.sn[s].n), 0});
+      }
+    if (t.empty()) continue;
+    SolveLevel L;
+    L.ntask = int(t.size());
+    L.d_tasks = upload(t);
+    L.ntask32 = int(t32.size());
+    L.d_tasks32 = upload(t32);
+    plan.bwd.push_back(L);
+  }
+  // segment-table bounds (per-warp shared scratch of the row pulls)
+  int seg_sub = 1, seg_top = 1;
+  for (int p = 0; p < Y.n; ++p) {
+    const int ns = Y.seg_ptr[p + 1] - Y.seg_ptr[p];
+    const int sn = Y.sn_of_pos[p];
+    if (sn < 0) continue;
+    if (root_of[sn] >= 0) seg_sub = std::max(seg_sub, ns); else seg_top = std::max(seg_top, ns);
+  }
+  plan.sub.seg_max = seg_sub;
+  plan.seg_max_top = seg_top;
+}
+
 // ----------------------------------------------------------------- factorization
 void hddm_engine::factorize() {
   const auto t0 = now_ms();
@@ -505,8 +626,11 @@ SolveArgs hddm_engine::solve_args(const cplx* Bp, cplx* X, cplx* Yp) {
   A.blk = d_blk;
   A.row_first = d_row_first;
   A.row_off = d_row_off;
-  A.rin_ptr = d_rin_ptr;
-  A.rin = d_rin;
+  A.run_off = d_run_off;
+  A.seg_ptr = d_seg_ptr;
+  A.seg = d_seg;
+  A.bw_ptr = d_bw_ptr;
+  A.bw = d_bw;
   A.vals = d_vals;
   A.nvals = Y.nvals;
   A.act_ptr = d_act_ptr;
@@ -546,7 +670,7 @@ void hddm_engine::run_probe() {
   CK(cudaMemcpyAsync(d_act_ptr, aptr.data(), sizeof(int) * (ncls + 1), cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_act_list, alist.data(), sizeof(int) * ncls, cudaMemcpyHostToDevice, st));
   CK(cudaStreamSynchronize(st));
-  launch_solve(solve_args(d_B, d_U[0], d_Y), plan, ncls, 1, st);
+  launch_solve(solve_args(d_B, d_U[0], d_Y), plan, ncls, 1, ncls, st);
   CheckArgs C;
   C.nw = nw;
   C.wnx = wnx;
@@ -651,7 +775,7 @@ void hddm_engine::enqueue_step(int s, const cplx* f) {
   launch_gather(A, st);
   stage_end(0);
   stage_begin(1);
-  launch_solve(solve_args(d_B, A.Ucur, d_Y), plan, ncls, max_members, st);
+  launch_solve(solve_args(d_B, A.Ucur, d_Y), plan, ncls, max_members, nsub, st);
   stage_end(1);
   stage_begin(2);
   CheckArgs C;
@@ -681,8 +805,9 @@ void hddm_engine::enqueue_step(int s, const cplx* f) {
   stage_begin(3);
   launch_accumulate(A, st);
   stage_end(3);
-  if (timing)
-    for (int k = 0; k < 4; ++k) stage_collect(k);
+  launches += 2 + solve_launches() + 2 + 1;
+  // bound the pending event list inside long runs
+  if (timing && ev_next > 4096) stage_resolve();
   last_step = s;
 }
 
@@ -912,6 +1037,7 @@ int hddm_precondition(hddm_engine* e, const double* r, double* z, int ksteps, in
     CK(cudaMemsetAsync(e->d_refine, 0, sizeof(int), e->st));
     StepArgs A0 = e->step_args(1, dr);
     launch_fany(A0, e->st);
+    e->launches += 4;  // 3 flag fills + fany
     for (int s = 1; s <= ksteps; ++s) e->enqueue_step(s, dr);
     out_copy(e, z, e->d_asm, memkind);
     long long cnt[2];
@@ -1091,7 +1217,7 @@ int hddm_class_solve(hddm_engine* e, int c, const double* b, double* x, double* 
     CK(cudaMemcpyAsync(e->d_Z[0], zc.data(), sizeof(int) * e->nsub, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(e->d_act_ptr, aptr.data(), sizeof(int) * (e->ncls + 1), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(e->d_act_list, alist.data(), sizeof(int), cudaMemcpyHostToDevice, st));
-    launch_solve(e->solve_args(e->d_B, e->d_U[0], e->d_Y), e->plan, e->ncls, 1, st);
+    launch_solve(e->solve_args(e->d_B, e->d_U[0], e->d_Y), e->plan, e->ncls, 1, 1, st);
     CheckArgs C;
     C.nw = e->nw;
     C.wnx = e->wnx;
@@ -1131,16 +1257,29 @@ int hddm_class_solve(hddm_engine* e, int c, const double* b, double* x, double* 
 }
 
 int hddm_set_timing(hddm_engine* e, int enable) {
-  e->timing = enable != 0;
-  for (double& v : e->stage_ms) v = 0;
-  return HDDM_OK;
+  return guarded(e, [&] {
+    e->stage_resolve();
+    e->timing = enable != 0;
+    for (int k = 0; k < kStages; ++k) {
+      e->stage_ms[k] = 0;
+      e->stage_n[k] = 0;
+    }
+    e->launches = 0;
+  });
 }
 
-int hddm_stage_times(const hddm_engine* e, double* ms, int cap, int* n) {
-  for (int k = 0; k < kStages && k < cap; ++k) ms[k] = e->stage_ms[k];
-  *n = kStages;
-  return HDDM_OK;
+int hddm_stage_times(hddm_engine* e, double* ms, long long* count, int cap, int* n) {
+  return guarded(e, [&] {
+    e->stage_resolve();
+    for (int k = 0; k < kStages && k < cap; ++k) {
+      ms[k] = e->stage_ms[k];
+      if (count) count[k] = e->stage_n[k];
+    }
+    *n = kStages;
+  });
 }
+
+long long hddm_launch_count(const hddm_engine* e) { return e->launches; }
 
 const char* hddm_stage_name(int i) { return i >= 0 && i < kStages ? kStageNames[i] : ""; }
 

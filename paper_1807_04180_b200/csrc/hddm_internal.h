@@ -56,6 +56,15 @@ struct Symbolic {
   std::vector<Block> blk;
   std::vector<int> row_first;        // per block/band row: first column (relative)
   std::vector<long> row_off;         // per block/band row: value offset
+  // forward runs: incoming entries of factor-order position p are the values
+  // [run_off[p], run_off[p+1]), split into segments seg[seg_ptr[p]..seg_ptr[p+1])
+  // of (length, first source position)
+  struct Seg {
+    int len, zbase;
+  };
+  std::vector<long> run_off;
+  std::vector<int> seg_ptr;
+  std::vector<Seg> seg;
   long nvals = 0;                    // complex values per class
   long nnz_ref = 0;                  // reference's factor_nonzeros() (nnz(L) + n)
   long nnz_stored = 0;               // strictly-lower entries actually stored

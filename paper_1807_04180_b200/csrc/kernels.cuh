@@ -13,8 +13,11 @@ struct SolveArgs {
   const DevBlk* blk;
   const int* row_first;
   const long long* row_off;
-  const int* rin_ptr;  // per factor-order position: incoming forward entries
-  const RowIn* rin;
+  const long long* run_off;  // per position: incoming run [run_off[p], run_off[p+1])
+  const int* seg_ptr;        // per position: segments of the run
+  const int2* seg;           // (length, first source position)
+  const int* bw_ptr;         // per supernode: backward rows
+  const BwRow* bw;
   const cplx* vals;    // ncls x nvals
   long long nvals;
   const int* act_ptr;  // CSR over classes of right-hand-side ids
@@ -28,16 +31,44 @@ struct SolveArgs {
 struct SolveLevel {
   int ntask = 0;
   Task* d_tasks = nullptr;
+  int ntask32 = 0;          // backward pull: 32-column tasks
+  Task* d_tasks32 = nullptr;
+};
+
+// a maximal ND subtree solved by one CTA: positions [p0, p0+np), phases
+// [ph0, ph0+nph) bottom-up
+struct SubtreeInfo {
+  int p0, np, ph0, nph;
+};
+struct Phase {
+  int kind, it0, nit, pad;  // kind 0 leaves (items (leaf, 0)), 1 separators (items (sn, i))
+  int ic0, nic, pad1, pad2; // kind 0: leaf columns (items (leaf, j)) for the backward blocks
+};
+struct SubtreeArgs {
+  const SubtreeInfo* st;
+  const Phase* ph;
+  const int2* items;
+  int np_max, items_max, seg_max;
+};
+// classes grouped by member count; MC = members per shared-memory pass
+struct SolveBucket {
+  int mc = 1, ncls = 0;
+  int* d_cls = nullptr;
 };
 
 struct SolvePlan {
-  int nleaf = 0;
-  int* d_leaves = nullptr;
-  std::vector<SolveLevel> fwd, bwd;
+  int* d_wprefix = nullptr;  // per class: first warp of the (class, subtree, rhs) list
+  int nsubtree = 0;
+  SubtreeArgs sub{};
+  std::vector<SolveBucket> buckets;
+  std::vector<SolveLevel> fwd, bwd;  // separators above the subtrees
+  int seg_max_top = 0;               // most segments of any top-level row
 };
 
+// max_rhs bounds the number of active right-hand sides over all classes
 void launch_solve(const SolveArgs& A, const SolvePlan& P, int ncls, int max_members,
-                  cudaStream_t st);
+                  int max_rhs, cudaStream_t st);
+int solve_launch_count(const SolvePlan& P);
 
 // ------------------------------------------------------------------ factor
 struct FactorArgs {

@@ -190,27 +190,17 @@ void build_symbolic(int nx, int ny, Symbolic& S) {
   S.blk.clear();
   S.row_first.clear();
   S.row_off.clear();
-  long off = 0;
   S.nnz_stored = 0;
   for (int s = 0; s < nsn; ++s) {
     SnNode& nd = S.sn[s];
-    nd.dinv_off = off;
-    off += nd.n;
-    nd.diag_off = off;
-    if (nd.kind == 1) {
-      off += long(nd.n) * (nd.n - 1) / 2;
-      S.nnz_stored += long(nd.n) * (nd.n - 1) / 2;
-    } else {
+    if (nd.kind == 0) {
       nd.drow0 = int(S.row_first.size());
       for (int i = 0; i < nd.n; ++i) {
         const int k = nd.c0 + i;
         const int f = band_first[k] < 0 ? nd.n : band_first[k] - nd.c0;
         // contiguous profile assumed; padding keeps correctness otherwise
         S.row_first.push_back(std::min(f, i));
-        S.row_off.push_back(off);
-        const int len = i - std::min(f, i);
-        off += len;
-        S.nnz_stored += len;
+        S.row_off.push_back(0);
       }
     }
     nd.blk0 = int(S.blk.size());
@@ -237,9 +227,7 @@ void build_symbolic(int nx, int ny, Symbolic& S) {
           ++c;
         }
         S.row_first.push_back(first);
-        S.row_off.push_back(off);
-        off += nd.n - first;
-        S.nnz_stored += nd.n - first;
+        S.row_off.push_back(0);
         nd.rows.push_back(r);
       }
       S.blk.push_back(B);
@@ -247,6 +235,52 @@ void build_symbolic(int nx, int ny, Symbolic& S) {
     }
     nd.nblk = int(S.blk.size()) - nd.blk0;
   }
+  // incoming rows per destination position, in source (postorder) order
+  std::vector<std::vector<int>> incoming(n);
+  for (const Block& B : S.blk)
+    for (int r = 0; r < B.nr; ++r) incoming[S.sn[B.dst].c0 + B.r0 + r].push_back(B.row0 + r);
+  // value layout per supernode: [1/D | diagonal part | incoming runs of its rows]
+  // -- every separator row's incoming entries form ONE contiguous run, so the
+  // forward pull streams it; the backward reads each block row (a piece of some
+  // ancestor's run) through the row table.
+  long off = 0;
+  S.run_off.assign(n + 1, 0);
+  S.seg_ptr.assign(n + 1, 0);
+  S.seg.clear();
+  for (int s = 0; s < nsn; ++s) {
+    SnNode& nd = S.sn[s];
+    nd.dinv_off = off;
+    off += nd.n;
+    nd.diag_off = off;
+    if (nd.kind == 1) {
+      off += long(nd.n) * (nd.n - 1) / 2;
+      S.nnz_stored += long(nd.n) * (nd.n - 1) / 2;
+    } else {
+      for (int i = 0; i < nd.n; ++i) {
+        const int rt = nd.drow0 + i;
+        S.row_off[rt] = off;
+        off += i - S.row_first[rt];
+        S.nnz_stored += i - S.row_first[rt];
+      }
+    }
+  }
+  std::vector<int> src_of(S.row_first.size(), -1);
+  for (size_t b = 0; b < S.blk.size(); ++b)
+    for (int r = 0; r < S.blk[b].nr; ++r) src_of[S.blk[b].row0 + r] = S.blk[b].src;
+  for (int pos = 0; pos < n; ++pos) {
+    S.run_off[pos] = off;
+    S.seg_ptr[pos] = int(S.seg.size());
+    for (int rt : incoming[pos]) {
+      const SnNode& src = S.sn[src_of[rt]];
+      const int len = src.n - S.row_first[rt];
+      S.row_off[rt] = off;
+      if (len > 0) S.seg.push_back({len, src.c0 + S.row_first[rt]});
+      off += len;
+      S.nnz_stored += len;
+    }
+  }
+  S.run_off[n] = off;
+  S.seg_ptr[n] = int(S.seg.size());
   S.nvals = off;
 
   // fronts, extend-add maps, A scatter lists

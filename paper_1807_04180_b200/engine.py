@@ -141,7 +141,8 @@ def load_library(path: str = LIB_PATH):
         "hddm_nd_order": (C.c_int, [C.c_int, C.c_int, ip]),
         "hddm_footprint": (C.c_int, [vp, P(C.c_long), P(C.c_long), P(C.c_long)]),
         "hddm_set_timing": (C.c_int, [vp, C.c_int]),
-        "hddm_stage_times": (C.c_int, [vp, dp, C.c_int, ip]),
+        "hddm_stage_times": (C.c_int, [vp, dp, P(C.c_longlong), C.c_int, ip]),
+        "hddm_launch_count": (C.c_longlong, [vp]),
         "hddm_stage_name": (C.c_char_p, [C.c_int]),
         "hddm_stream": (vp, [vp]),
     }
@@ -382,11 +383,18 @@ class DdmEngine:
         self._check(self.lib.hddm_set_timing(self.h, 1 if on else 0))
 
     def stage_times(self):
+        """{stage: (total device ms, number of timed instances)} since set_timing."""
         buf = np.zeros(16, np.float64)
+        cnt = np.zeros(16, np.int64)
         n = C.c_int()
-        self.lib.hddm_stage_times(self.h, buf.ctypes.data_as(C.POINTER(C.c_double)), 16,
-                                  C.byref(n))
-        return {self.lib.hddm_stage_name(i).decode(): float(buf[i]) for i in range(n.value)}
+        self._check(self.lib.hddm_stage_times(self.h, buf.ctypes.data_as(C.POINTER(C.c_double)),
+                                              cnt.ctypes.data_as(C.POINTER(C.c_longlong)), 16,
+                                              C.byref(n)))
+        return {self.lib.hddm_stage_name(i).decode(): (float(buf[i]), int(cnt[i]))
+                for i in range(n.value)}
+
+    def launch_count(self) -> int:
+        return int(self.lib.hddm_launch_count(self.h))
 
     def stream_handle(self) -> int:
         return int(self.lib.hddm_stream(self.h) or 0)
