@@ -144,6 +144,11 @@ int hddm_class_solve(hddm_engine* e, int c, const double* b, double* x,
 /* Window node counts and the reference elimination order (perm[pos] = node). */
 int hddm_window_dims(const hddm_engine* e, int* nx, int* ny);
 int hddm_nd_order(int nx, int ny, int* order);
+/* Host-only symbolic analysis of an nx-by-ny window (no GPU needed):
+ * the reference's factor_nonzeros() (nnz(L)+n, sparse.cpp:238-240), the
+ * strictly-lower entries the engine stores, supernode count, tree height. */
+int hddm_symbolic_stats(int nx, int ny, long* nnz_ref, long* stored, int* nsuper,
+                        int* height);
 /* Symbolic/footprint figures: stored factor values per class, the
  * reference's nnz(L)+n per class, total device bytes held by the engine. */
 int hddm_footprint(const hddm_engine* e, long* stored_per_class,

@@ -44,6 +44,13 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 __device__ __forceinline__ cplx ldg(const cplx* p) { return __ldg(p); }
 
+// Asynchronous bulk prefetch of a contiguous global range into L2 (TMA path,
+// sm_90+). p must be 16-byte aligned and bytes a multiple of 16.
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  if (bytes == 0) return;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // ------------------------------------------------------------ device tables
 struct DevSn {
   int kind, c0, n, nrows;

@@ -15,6 +15,7 @@
 #include <complex>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -83,6 +84,7 @@ struct hddm_engine {
   long long* d_run_off = nullptr;
   int* d_seg_ptr = nullptr;
   int2* d_seg = nullptr;
+  int* d_zidx = nullptr;
   int* d_bw_ptr = nullptr;
   BwRow* d_bw = nullptr;
   int* d_perm = nullptr;
@@ -117,6 +119,9 @@ struct hddm_engine {
   cplx* d_asm = nullptr;
   cplx* d_tmp = nullptr;
   int* d_colcov = nullptr;
+  int* d_pnode = nullptr;
+  int* d_pmask = nullptr;
+  int npatch = 0;
   int* d_rowcov = nullptr;
   double* d_part = nullptr;
   double* d_scal = nullptr;  // small scalars
@@ -219,7 +224,14 @@ struct hddm_engine {
 
 // ----------------------------------------------------------------- creation
 void hddm_engine::create(const hddm_problem& p) {
+  // configuration errors first (the reference's constructor validates the
+  // partition before anything else, partition.cpp:15-28)
+  std::string msg;
+  const int rc = build_setup(p, S, msg);
+  if (rc == HDDM_ERR_CONFIG) throw ConfigErr(msg);
+  if (rc) throw std::runtime_error(msg);
   int ndev = 0;
+  dev = -1;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     throw std::runtime_error("no CUDA device available (the engine has no CPU fallback)");
   dev = p.device;
@@ -227,10 +239,6 @@ void hddm_engine::create(const hddm_problem& p) {
   CK(cudaSetDevice(dev));
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   CK(cudaMallocHost(&h_scal, 64 * sizeof(double)));
-  std::string msg;
-  const int rc = build_setup(p, S, msg);
-  if (rc == HDDM_ERR_CONFIG) throw ConfigErr(msg);
-  if (rc) throw std::runtime_error(msg);
   nsub = S.n1 * S.n2;
   ncls = S.ncls;
   wnx = S.subs[0].nx;
@@ -283,6 +291,13 @@ void hddm_engine::create(const hddm_problem& p) {
     std::vector<int2> sg(Y.seg.size());
     for (size_t k = 0; k < Y.seg.size(); ++k) sg[k] = make_int2(Y.seg[k].len, Y.seg[k].zbase);
     d_seg = upload(sg);
+    std::vector<int> zi(Y.nvals, 0);
+    for (int p = 0; p < Y.n; ++p) {
+      long o = Y.run_off[p];
+      for (int k = Y.seg_ptr[p]; k < Y.seg_ptr[p + 1]; ++k)
+        for (int j = 0; j < Y.seg[k].len; ++j) zi[o++] = Y.seg[k].zbase + j;
+    }
+    d_zidx = upload(zi);
     std::vector<int> bptr(Y.sn.size() + 1, 0);
     std::vector<BwRow> bw;
     for (size_t s = 0; s < Y.sn.size(); ++s) {
@@ -409,11 +424,44 @@ void hddm_engine::create(const hddm_problem& p) {
     d_colcov = upload(colcov);
     d_rowcov = upload(rowcov);
   }
+  // union of the transfer patches in window-local coordinates
+  // (transfer_patch, transfer.cpp:7-62; identical for every window)
+  {
+    const Sub& s0 = S.subs[0];
+    const int ext = S.ext, nov = S.nov;
+    const int cx0 = ext, cx1 = ext + S.mcx, cy0 = ext, cy1 = ext + S.mcy;
+    std::vector<int> mask(size_t(wnx) * wny, 0);
+    for (int d = 0; d < 8; ++d) {
+      int p0 = 1, p1 = wnx - 2, q0 = 1, q1 = wny - 2;
+      const bool fL = d == 1 || d == 5 || d == 7, fR = d == 0 || d == 4 || d == 6;
+      const bool fB = d == 3 || d == 6 || d == 7, fT = d == 2 || d == 4 || d == 5;
+      if (fL) { p0 = std::max(p0, cx0 + 1); p1 = std::min(p1, cx0 + 1 + nov); }
+      if (fR) { p0 = std::max(p0, cx1 - 1 - nov); p1 = std::min(p1, cx1 - 1); }
+      if (fB) { q0 = std::max(q0, cy0 + 1); q1 = std::min(q1, cy0 + 1 + nov); }
+      if (fT) { q0 = std::max(q0, cy1 - 1 - nov); q1 = std::min(q1, cy1 - 1); }
+      for (int q = q0; q <= q1; ++q)
+        for (int pp = p0; pp <= p1; ++pp) mask[size_t(q) * wnx + pp] |= 1 << d;
+    }
+    (void)s0;
+    std::vector<int> pn, pm;
+    for (int k = 0; k < nw; ++k) {  // factor order: coalesced writes of B
+      const int node = Y.perm[k];
+      if (mask[node]) {
+        pn.push_back(node);
+        pm.push_back(mask[node]);
+      }
+    }
+    npatch = int(pn.size());
+    d_pnode = upload(pn);
+    d_pmask = upload(pm);
+  }
   d_part = dalloc<double>(2 * size_t(reduce_blocks()));
   d_scal = dalloc<double>(64);
 
   factorize();
   run_probe();
+  // profiling knob: skip subtree phase kinds in DDM steps (results invalid)
+  if (const char* dbg = std::getenv("HDDM_DEBUG_SKIP")) plan.sub.dbg = std::atoi(dbg);
 }
 
 // Solve plan: maximal subtrees of at most kSubtreeMax nodes run as one CTA each
@@ -629,6 +677,7 @@ SolveArgs hddm_engine::solve_args(const cplx* Bp, cplx* X, cplx* Yp) {
   A.run_off = d_run_off;
   A.seg_ptr = d_seg_ptr;
   A.seg = d_seg;
+  A.zidx = d_zidx;
   A.bw_ptr = d_bw_ptr;
   A.bw = d_bw;
   A.vals = d_vals;
@@ -722,6 +771,11 @@ StepArgs hddm_engine::step_args(int s, const cplx* f) {
   A.wny = wny;
   A.nw = nw;
   A.nring = Y.nring;
+  A.mcx = S.mcx;
+  A.mcy = S.mcy;
+  A.npatch = npatch;
+  A.pnode = d_pnode;
+  A.pmask = d_pmask;
   A.ih2 = 1.0 / (S.h * S.h);
   A.sub = d_sub;
   A.sa = d_sa;
@@ -805,7 +859,7 @@ void hddm_engine::enqueue_step(int s, const cplx* f) {
   stage_begin(3);
   launch_accumulate(A, st);
   stage_end(3);
-  launches += 2 + solve_launches() + 2 + 1;
+  launches += 3 + solve_launches() + 2 + 1;
   // bound the pending event list inside long runs
   if (timing && ev_next > 4096) stage_resolve();
   last_step = s;
@@ -888,6 +942,7 @@ void read_counts(hddm_engine* e, long long* c) {
 }
 
 void check_refine(hddm_engine* e) {
+  if (e->plan.sub.dbg) return;  // profiling knob active: results are invalid by design
   int flag = 0;
   CK(cudaMemcpyAsync(&flag, e->d_refine, sizeof(int), cudaMemcpyDeviceToHost, e->st));
   CK(cudaStreamSynchronize(e->st));
@@ -942,6 +997,18 @@ int hddm_nd_order(int nx, int ny, int* order) {
   const std::vector<int> o = nd_order(nx, ny);
   std::copy(o.begin(), o.end(), order);
   return HDDM_OK;
+}
+
+int hddm_symbolic_stats(int nx, int ny, long* nnz_ref, long* stored, int* nsuper,
+                        int* height) {
+  return guarded(nullptr, [&] {
+    Symbolic S;
+    build_symbolic(nx, ny, S);
+    *nnz_ref = long(S.nnz_ref);
+    *stored = long(S.nnz_stored);
+    *nsuper = int(S.sn.size());
+    *height = S.max_height;
+  });
 }
 
 int hddm_footprint(const hddm_engine* e, long* stored, long* ref_nnz, long* device_bytes) {

@@ -16,6 +16,7 @@ struct SolveArgs {
   const long long* run_off;  // per position: incoming run [run_off[p], run_off[p+1])
   const int* seg_ptr;        // per position: segments of the run
   const int2* seg;           // (length, first source position)
+  const int* zidx;           // per run value: source position (structural, all classes)
   const int* bw_ptr;         // per supernode: backward rows
   const BwRow* bw;
   const cplx* vals;    // ncls x nvals
@@ -49,6 +50,7 @@ struct SubtreeArgs {
   const Phase* ph;
   const int2* items;
   int np_max, items_max, seg_max;
+  int dbg;  // profiling only (HDDM_DEBUG_SKIP): bit0/1 skip fwd leaf/sep phases, bit2/3 bwd
 };
 // classes grouped by member count; MC = members per shared-memory pass
 struct SolveBucket {
@@ -94,7 +96,10 @@ void launch_factor_level(const FactorArgs& A, const int* d_nodes, int nnodes, in
 // ------------------------------------------------------------------ DDM step
 struct StepArgs {
   // geometry
-  int n1, n2, nsub, nov, gnx, gny, wnx, wny, nw, nring;
+  int n1, n2, nsub, nov, gnx, gny, wnx, wny, nw, nring, mcx, mcy;
+  int npatch;            // structural union of the 8 transfer patches (window nodes)
+  const int* pnode;
+  const int* pmask;      // bit d: node lies in direction d's patch
   double ih2;
   const DevSub* sub;
   const cplx* sa;        // per-sub alpha arrays: a1n[wnx] ia1h[wnx] a2n[wny] ia2h[wny]

@@ -135,64 +135,105 @@ __device__ __forceinline__ bool in_patch(int d, const DevSub& T, int wnx, int wn
 
 }  // namespace
 
-__global__ void __launch_bounds__(256) k_gather(StepArgs A) {
+// Right-hand side assembly in two passes (restrict_owned + add_transfer +
+// scale_rhs, ddm.cpp:183-205, transfer.cpp:64-88, discretize.cpp:162-172):
+//  (1) every window node: B = J * f_owned (step 1) or 0; ring rows 0;
+//  (2) only nodes of the union of the 8 transfer patches (a structural list,
+//      identical for every window): B = J * (f_owned - sum_d L_t(beta_d v_d))
+//      over the in-range, non-zero-flagged sources in kGatherOrder.
+__global__ void __launch_bounds__(256) k_rhs_base(StepArgs A) {
   const int t = blockIdx.y;
   if (A.zc[t]) return;
   const int pos = blockIdx.x * blockDim.x + threadIdx.x;
   if (pos >= A.nw) return;
   cplx* Bt = A.B + (long long)t * A.nw;
-  const int node = A.perm[pos];
-  const int lp = node % A.wnx, lq = node / A.wnx;
-  if (lp == 0 || lq == 0 || lp == A.wnx - 1 || lq == A.wny - 1) {
-    Bt[pos] = cmk(0, 0);
-    return;
+  cplx v = cmk(0, 0);
+  if (A.step == 1) {
+    const int node = A.perm[pos];
+    const int lp = node % A.wnx, lq = node / A.wnx;
+    if (lp > 0 && lq > 0 && lp < A.wnx - 1 && lq < A.wny - 1) {
+      const DevSub T = A.sub[t];
+      const int P = T.wx0 + lp, Q = T.wy0 + lq;
+      if (P >= T.own0 && P <= T.own1 && Q >= T.own2 && Q <= T.own3) {
+        const cplx* sa = A.sa + (long long)t * A.sa_stride;
+        v = cmul(cmul(sa[lp], sa[2 * A.wnx + lq]), A.f[(long long)Q * A.gnx + P]);
+      }
+    }
   }
+  Bt[pos] = v;
+}
+
+__global__ void __launch_bounds__(256) k_rhs_transfer(StepArgs A) {
+  const int t = blockIdx.y;
+  if (A.zc[t]) return;
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= A.npatch) return;
+  const int node = A.pnode[u];
+  const int mask = A.pmask[u];
+  const int lp = node % A.wnx, lq = node / A.wnx;
   const DevSub T = A.sub[t];
   const int P = T.wx0 + lp, Q = T.wy0 + lq;
   const cplx* sa = A.sa + (long long)t * A.sa_stride;
-  const cplx* a1n = sa;
-  const cplx* ia1h = sa + A.wnx;
-  const cplx* a2n = sa + 2 * A.wnx;
-  const cplx* ia2h = sa + 2 * A.wnx + A.wny;
-  const cplx jac = cmul(a1n[lp], a2n[lq]);
+  const cplx a1 = sa[lp], a2 = sa[2 * A.wnx + lq];
+  const cplx ia1w = sa[A.wnx + lp - 1], ia1e = sa[A.wnx + lp];
+  const cplx ia2s = sa[2 * A.wnx + A.wny + lq - 1], ia2n = sa[2 * A.wnx + A.wny + lq];
+  const cplx jac = cmul(a1, a2);
+  const double k2 = A.k2[(long long)Q * A.gnx + P];
+  const cplx ex = cscale(a2, A.ih2), ey = cscale(a1, A.ih2);
+  const cplx cE = cmul(ex, ia1e), cW = cmul(ex, ia1w), cN = cmul(ey, ia2n), cS = cmul(ey, ia2s);
   cplx val = cmk(0, 0);
   if (A.step == 1 && P >= T.own0 && P <= T.own1 && Q >= T.own2 && Q <= T.own3)
     val = A.f[(long long)Q * A.gnx + P];
-  const double k2 = A.k2[(long long)Q * A.gnx + P];
+  bool any = false;
   for (int d = 0; d < 8; ++d) {
-    const int si = T.i + kDI[d], sj = T.j + kDJ[d];
+    if (!((mask >> d) & 1)) continue;
+    const int di = kDI[d], dj = kDJ[d];
+    const int si = T.i + di, sj = T.j + dj;
     if (si < 0 || si >= A.n1 || sj < 0 || sj >= A.n2) continue;
     const int src = sj * A.n1 + si;
     const bool corner = d >= 4;
     if ((corner ? A.zp2 : A.zp1)[src]) continue;
-    if (!in_patch(d, T, A.wnx, A.wny, A.nov, P, Q)) continue;
-    const DevSub S = A.sub[src];
+    any = true;
     const cplx* V = (corner ? A.Up2 : A.Up1) + (long long)src * A.nw;
-    // w = beta_d * v_src (zero outside the source window) at the 5 stencil nodes
-    auto w = [&](int p, int q) -> cplx {
-      const int sp = p - S.wx0, sq = q - S.wy0;
-      if (sp < 0 || sq < 0 || sp >= A.wnx || sq >= A.wny) return cmk(0, 0);
-      const cplx v = V[A.pinv[sq * A.wnx + sp]];
-      if (v.x == 0.0 && v.y == 0.0) return cmk(0, 0);
-      return cscale(v, tbeta(d, T, A.nov, p, q));
-    };
-    const cplx uc = w(P, Q);
-    const cplx ex = cscale(a2n[lq], A.ih2);
-    const cplx ey = cscale(a1n[lp], A.ih2);
-    // DiscreteOperator::stencil (discretize.hpp:43-54), same operation order
-    cplx tt = cmul(cmul(ex, ia1h[lp]), csub(w(P + 1, Q), uc));
-    tt = csub(tt, cmul(cmul(ex, ia1h[lp - 1]), csub(uc, w(P - 1, Q))));
-    tt = cadd(tt, cmul(cmul(ey, ia2h[lq]), csub(w(P, Q + 1), uc)));
-    tt = csub(tt, cmul(cmul(ey, ia2h[lq - 1]), csub(uc, w(P, Q - 1))));
-    const cplx Lw = cadd(cdiv(tt, jac), cscale(uc, k2));
-    val = csub(val, Lw);
+    // source-local coordinates of the target node: windows are offset by whole cores
+    const int sp = lp - di * A.mcx, sq = lq - dj * A.mcy;
+    const bool fromL = d == 1 || d == 5 || d == 7, fromR = d == 0 || d == 4 || d == 6;
+    const bool fromB = d == 3 || d == 6 || d == 7, fromT = d == 2 || d == 4 || d == 5;
+    cplx w5[5];  // C, E, W, N, S
+    const int dp[5] = {0, 1, -1, 0, 0}, dq[5] = {0, 0, 0, 1, -1};
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const int xp = sp + dp[k], xq = sq + dq[k];
+      cplx v = cmk(0, 0);
+      if (xp >= 0 && xq >= 0 && xp < A.wnx && xq < A.wny) v = V[A.pinv[xq * A.wnx + xp]];
+      if (v.x != 0.0 || v.y != 0.0) {
+        // transfer_beta (partition.cpp:131-152) at the global node
+        const int p = P + dp[k], q = Q + dq[k];
+        double b = 1.0;
+        if (fromL) b = beta0(double(p - T.cx0 - 1) / A.nov);
+        if (fromR) b = beta0(double(T.cx1 - 1 - p) / A.nov);
+        if (fromB) b *= beta0(double(q - T.cy0 - 1) / A.nov);
+        if (fromT) b *= beta0(double(T.cy1 - 1 - q) / A.nov);
+        v = cscale(v, b);
+      }
+      w5[k] = v;
+    }
+    const cplx uc = w5[0];
+    // DiscreteOperator::stencil (discretize.hpp:43-54)
+    cplx tt = cmul(cE, csub(w5[1], uc));
+    tt = csub(tt, cmul(cW, csub(uc, w5[2])));
+    tt = cadd(tt, cmul(cN, csub(w5[3], uc)));
+    tt = csub(tt, cmul(cS, csub(uc, w5[4])));
+    val = csub(val, cadd(cdiv(tt, jac), cscale(uc, k2)));
   }
-  Bt[pos] = cmul(jac, val);  // scale_rhs (discretize.cpp:162-172)
+  if (any) A.B[(long long)t * A.nw + A.pinv[node]] = cmul(jac, val);
 }
 
 void launch_gather(const StepArgs& A, cudaStream_t st) {
   dim3 g((A.nw + 255) / 256, A.nsub);
-  k_gather<<<g, 256, 0, st>>>(A);
+  k_rhs_base<<<g, 256, 0, st>>>(A);
+  dim3 g2((A.npatch + 255) / 256, A.nsub);
+  k_rhs_transfer<<<g2, 256, 0, st>>>(A);
 }
 
 // ------------------------------------------------------------ accumulate

@@ -76,24 +76,57 @@ __device__ __forceinline__ cplx bw_dot(const cplx* __restrict__ vals, const BwRo
                                        int nrows, int j, XGet xget) {
   cplx acc = cmk(0, 0);
   int k = 0;
-  for (; k + 4 <= nrows; k += 4) {
-    BwRow d[4];
-    cplx l[4], x[4];
+  constexpr int U = 8;
+  for (; k + U <= nrows; k += U) {
+    BwRow d[U];
+    cplx l[U], x[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) d[u] = rows[k + u];
+    for (int u = 0; u < U; ++u) d[u] = rows[k + u];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       l[u] = j >= d[u].first ? ldg(vals + d[u].off + (j - d[u].first)) : cmk(0, 0);
       x[u] = xget(d[u].dpos);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) cfma(acc, l[u], x[u]);
+    for (int u = 0; u < U; ++u) cfma(acc, l[u], x[u]);
   }
   for (; k < nrows; ++k) {
     const BwRow d = rows[k];
     if (j >= d.first) cfma(acc, ldg(vals + d.off + (j - d.first)), xget(d.dpos));
   }
   return acc;
+}
+
+// L2 prefetch of the factor data phase ph will read (forward: the leaves'
+// bands / the separators' incoming runs and inverses; backward: the rows of the
+// phase's supernodes and their inverses). Issued one phase ahead.
+__device__ __forceinline__ void prefetch_phase(const SolveArgs& A, const SubtreeArgs& T,
+                                               const cplx* vals, int ph, bool fwd, int lane) {
+  const Phase P = T.ph[ph];
+  const int2* items = T.items + P.it0;
+  for (int q = lane; q < P.nit; q += 32) {
+    const int2 it = items[q];
+    if (P.kind == 1 && it.y != 0) continue;  // one entry per separator
+    const DevSn sn = A.sn[it.x];
+    if (sn.kind == 0) {
+      // [1/D | band] is contiguous
+      const long long e = A.row_off[sn.drow0 + sn.n - 1] + (sn.n - 1 - A.row_first[sn.drow0 + sn.n - 1]);
+      if (fwd) prefetch_l2(vals + sn.dinv_off, unsigned((e - sn.dinv_off) * sizeof(cplx)));
+    } else {
+      const long long e = sn.diag_off + (long long)sn.n * (sn.n - 1) / 2;
+      prefetch_l2(vals + sn.dinv_off, unsigned((e - sn.dinv_off) * sizeof(cplx)));
+      if (fwd) {
+        const long long r0 = A.run_off[sn.c0], r1 = A.run_off[sn.c0 + sn.n];
+        prefetch_l2(vals + r0, unsigned((r1 - r0) * sizeof(cplx)));
+      }
+    }
+    if (!fwd) {
+      for (int r = A.bw_ptr[it.x]; r < A.bw_ptr[it.x + 1]; ++r) {
+        const BwRow d = A.bw[r];
+        prefetch_l2(vals + d.off, unsigned((sn.n - d.first) * sizeof(cplx)));
+      }
+    }
+  }
 }
 
 }  // namespace
@@ -140,7 +173,7 @@ __device__ __forceinline__ size_t subtree_warp_words(const SubtreeArgs& T) {
   return (size_t)T.np_max + T.items_max + (T.seg_max + 1) / 2;
 }
 
-__global__ void __launch_bounds__(256, 2) k_fwd_subtree(SolveArgs A, SubtreeArgs T,
+__global__ void __launch_bounds__(256, 3) k_fwd_subtree(SolveArgs A, SubtreeArgs T,
                                                      const int* wprefix, int ncls) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -157,9 +190,11 @@ __global__ void __launch_bounds__(256, 2) k_fwd_subtree(SolveArgs A, SubtreeArgs
     for (int i = lane; i < np; i += 32) z[i] = src[i];
   }
   __syncwarp();
-  auto zget = [&](int pos) { return z[pos - p0]; };
+  prefetch_phase(A, T, vals, info.ph0, true, lane);
   for (int ph = info.ph0; ph < info.ph0 + info.nph; ++ph) {
+    if (ph + 1 < info.ph0 + info.nph) prefetch_phase(A, T, vals, ph + 1, true, lane);
     const Phase P = T.ph[ph];
+    if ((T.dbg >> (P.kind == 0 ? 0 : 1)) & 1) continue;
     const int2* items = T.items + P.it0;
     if (P.kind == 0) {
       // leaves: lane per leaf, band forward substitution
@@ -178,30 +213,52 @@ __global__ void __launch_bounds__(256, 2) k_fwd_subtree(SolveArgs A, SubtreeArgs
       __syncwarp();
       continue;
     }
-    // separator rows: y = b - (incoming run) . z, lane per row: every lane
-    // streams its own contiguous run, so a warp keeps up to 32 rows in flight
-    for (int it = lane; it < P.nit; it += 32) {
-      const int2 item = items[it];
-      const int pos = A.sn[item.x].c0 + item.y;
-      const cplx* run = vals + A.run_off[pos];
-      const int s0 = A.seg_ptr[pos], s1 = A.seg_ptr[pos + 1];
-      cplx acc = cmk(0, 0);
-      for (int k = s0; k < s1; ++k) {
-        const int2 sg = A.seg[k];
-        const cplx* zz = z + (sg.y - p0);
-        int jj = 0;
-        for (; jj + 4 <= sg.x; jj += 4) {
-          const cplx l0 = ldg(run + jj), l1 = ldg(run + jj + 1), l2 = ldg(run + jj + 2),
-                     l3 = ldg(run + jj + 3);
-          cfma(acc, l0, zz[jj]);
-          cfma(acc, l1, zz[jj + 1]);
-          cfma(acc, l2, zz[jj + 2]);
-          cfma(acc, l3, zz[jj + 3]);
+    // separator rows: y = b - (incoming run) . z. A warp walks four rows at a
+    // time with its lanes over the run elements (coalesced loads, eight
+    // independent global loads per lane per step); zidx gives each element's
+    // source position.
+    for (int g = 0; g < P.nit; g += 4) {
+      const cplx* run[4];
+      const int* zi[4];
+      int tot[4], pos[4];
+      int maxlen = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        tot[k] = 0;
+        pos[k] = -1;
+        if (g + k < P.nit) {
+          const int2 item = items[g + k];
+          pos[k] = A.sn[item.x].c0 + item.y;
+          const long long r0 = A.run_off[pos[k]];
+          run[k] = vals + r0;
+          zi[k] = A.zidx + r0;
+          tot[k] = int(A.run_off[pos[k] + 1] - r0);
+          maxlen = max(maxlen, tot[k]);
+        } else {
+          run[k] = vals;
+          zi[k] = A.zidx;
         }
-        for (; jj < sg.x; ++jj) cfma(acc, ldg(run + jj), zz[jj]);
-        run += sg.x;
       }
-      scr[it] = csub(z[pos - p0], acc);
+      cplx acc[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[k] = cmk(0, 0);
+      for (int q = lane; q < maxlen; q += 32) {
+        cplx l[4];
+        int ix[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const bool ok = q < tot[k];
+          l[k] = ok ? ldg(run[k] + q) : cmk(0, 0);
+          ix[k] = ok ? __ldg(zi[k] + q) - p0 : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) cfma(acc[k], l[k], z[ix[k]]);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const cplx sum = warp_sum(acc[k]);
+        if (lane == 0 && pos[k] >= 0) scr[g + k] = csub(z[pos[k] - p0], sum);
+      }
     }
     __syncwarp();
     for (int it = lane; it < P.nit; it += 32) {
@@ -233,7 +290,7 @@ __global__ void __launch_bounds__(256, 2) k_fwd_subtree(SolveArgs A, SubtreeArgs
   }
 }
 
-__global__ void __launch_bounds__(256, 2) k_bwd_subtree(SolveArgs A, SubtreeArgs T,
+__global__ void __launch_bounds__(256, 3) k_bwd_subtree(SolveArgs A, SubtreeArgs T,
                                                      const int* wprefix, int ncls) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -252,16 +309,22 @@ __global__ void __launch_bounds__(256, 2) k_bwd_subtree(SolveArgs A, SubtreeArgs
   };
   for (int ph = info.ph0 + info.nph - 1; ph >= info.ph0; --ph) {
     const Phase P = T.ph[ph];
+    if ((T.dbg >> (P.kind == 0 ? 2 : 3)) & 1) continue;
     if (P.kind == 0) {
-      // leaf columns: w_j = Dinv_j z_j - sum L[r][j] x_r, lane per column
-      const int2* cols = T.items + P.ic0;
-      for (int q = lane; q < P.nic; q += 32) {
-        const int2 it = cols[q];
-        const DevSn sn = A.sn[it.x];
-        const int j = it.y;
-        const int b0 = A.bw_ptr[it.x];
-        const cplx s = bw_dot(vals, A.bw + b0, A.bw_ptr[it.x + 1] - b0, j, xget);
-        z[sn.c0 + j - p0] = csub(cmul(ldg(vals + sn.dinv_off + j), z[sn.c0 + j - p0]), s);
+      // leaf columns: w_j = Dinv_j z_j - sum_r L[r][j] x_r, lane per column
+      // (lanes of one leaf read consecutive columns of each row: coalesced)
+      {
+        const int2* cols = T.items + P.ic0;
+        for (int q = lane; q < P.nic; q += 32) {
+          const int2 it = cols[q];
+          const DevSn sn = A.sn[it.x];
+          const int j = it.y;
+          const int b0 = A.bw_ptr[it.x];
+          const cplx sm = bw_dot(vals, A.bw + b0, A.bw_ptr[it.x + 1] - b0, j, xget);
+          // each (leaf, column) is owned by one lane and only reads x outside the
+          // leaf, so the update is in place
+          z[sn.c0 + j - p0] = csub(cmul(ldg(vals + sn.dinv_off + j), z[sn.c0 + j - p0]), sm);
+        }
       }
       __syncwarp();
       // band back-substitution, lane per leaf
@@ -314,11 +377,11 @@ __global__ void __launch_bounds__(256, 2) k_bwd_subtree(SolveArgs A, SubtreeArgs
 // ====================================================================== top levels
 
 // Forward pull for separator rows: Y[r] = B[r] - run . X (MR members per pass).
-// Warp per row; per-warp segment tables follow the member list in shared memory.
-__global__ void __launch_bounds__(256) k_fwd_pull(SolveArgs A, const Task* tasks, int seg_max,
-                                                  int max_members) {
-  extern __shared__ __align__(16) unsigned char s_raw[];
-  int* s_mem = reinterpret_cast<int*>(s_raw);
+// Warp per row, two run elements per lane per iteration; the source position of
+// every run element comes from the structural zidx array (shared by all
+// classes, so it stays L2-resident).
+__global__ void __launch_bounds__(256) k_fwd_pull(SolveArgs A, const Task* tasks) {
+  extern __shared__ int s_mem[];
   const int c = blockIdx.y;
   const int m = load_members(A, c, s_mem);
   if (m == 0) return;
@@ -326,31 +389,36 @@ __global__ void __launch_bounds__(256) k_fwd_pull(SolveArgs A, const Task* tasks
   const DevSn sn = A.sn[T.s];
   const cplx* vals = A.vals + (long long)c * A.nvals;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  int2* segs = reinterpret_cast<int2*>(s_raw + ((sizeof(int) * max_members + 15) & ~size_t(15))) +
-               (size_t)warp * seg_max;
   for (int r = T.a + warp; r < T.b; r += nwarp) {
     const int pos = sn.c0 + r;
-    const int ns = stage_segs(A, pos, segs, lane);
     const long long r0 = A.run_off[pos];
     const cplx* run = vals + r0;
+    const int* zi = A.zidx + r0;
     const int total = int(A.run_off[pos + 1] - r0);
     for (int mb = 0; mb < m; mb += MR) {
       const int mc = min(MR, m - mb);
       cplx acc[MR];
 #pragma unroll
       for (int k = 0; k < MR; ++k) acc[k] = cmk(0, 0);
-      int k2 = 0, segstart = 0;
-      int2 sg = ns > 0 ? segs[0] : make_int2(0, 0);
-      for (int q = lane; q < total; q += 32) {
-        while (q >= segstart + sg.x) {
-          segstart += sg.x;
-          sg = segs[++k2];
+      int q = lane;
+      for (; q + 32 < total; q += 64) {
+        const cplx l0 = ldg(run + q), l1 = ldg(run + q + 32);
+        const int i0 = __ldg(zi + q), i1 = __ldg(zi + q + 32);
+#pragma unroll
+        for (int k = 0; k < MR; ++k) {
+          if (k < mc) {
+            const cplx* Xk = A.X + (long long)s_mem[mb + k] * A.nw;
+            cfma(acc[k], l0, Xk[i0]);
+            cfma(acc[k], l1, Xk[i1]);
+          }
         }
-        const cplx l = ldg(run + q);
-        const int zi = sg.y + (q - segstart);
+      }
+      if (q < total) {
+        const cplx l0 = ldg(run + q);
+        const int i0 = __ldg(zi + q);
 #pragma unroll
         for (int k = 0; k < MR; ++k)
-          if (k < mc) cfma(acc[k], l, A.X[(long long)s_mem[mb + k] * A.nw + zi]);
+          if (k < mc) cfma(acc[k], l0, A.X[(long long)s_mem[mb + k] * A.nw + i0]);
       }
 #pragma unroll
       for (int k = 0; k < MR; ++k) {
@@ -363,7 +431,6 @@ __global__ void __launch_bounds__(256) k_fwd_pull(SolveArgs A, const Task* tasks
         }
       }
     }
-    __syncwarp();
   }
 }
 
@@ -426,13 +493,28 @@ __global__ void __launch_bounds__(256) k_bwd_pull(SolveArgs A, const Task* tasks
 #pragma unroll
     for (int k = 0; k < MR; ++k) acc[k] = cmk(0, 0);
     if (colok) {
-      for (int r = r0 + warp; r < r1; r += nwarp) {
-        const BwRow d = A.bw[r];
-        if (j < d.first) continue;
-        const cplx l = ldg(vals + d.off + (j - d.first));
+      int r = r0 + warp;
+      for (; r + nwarp < r1; r += 2 * nwarp) {
+        const BwRow d0 = A.bw[r], d1 = A.bw[r + nwarp];
+        const cplx l0 = j >= d0.first ? ldg(vals + d0.off + (j - d0.first)) : cmk(0, 0);
+        const cplx l1 = j >= d1.first ? ldg(vals + d1.off + (j - d1.first)) : cmk(0, 0);
 #pragma unroll
-        for (int k = 0; k < MR; ++k)
-          if (k < mc) cfma(acc[k], l, A.X[(long long)s_mem[mb + k] * A.nw + d.dpos]);
+        for (int k = 0; k < MR; ++k) {
+          if (k < mc) {
+            const cplx* Xk = A.X + (long long)s_mem[mb + k] * A.nw;
+            cfma(acc[k], l0, Xk[d0.dpos]);
+            cfma(acc[k], l1, Xk[d1.dpos]);
+          }
+        }
+      }
+      if (r < r1) {
+        const BwRow d = A.bw[r];
+        if (j >= d.first) {
+          const cplx l = ldg(vals + d.off + (j - d.first));
+#pragma unroll
+          for (int k = 0; k < MR; ++k)
+            if (k < mc) cfma(acc[k], l, A.X[(long long)s_mem[mb + k] * A.nw + d.dpos]);
+        }
       }
     }
 #pragma unroll
@@ -451,34 +533,46 @@ __global__ void __launch_bounds__(256) k_bwd_pull(SolveArgs A, const Task* tasks
 }
 
 // Backward diagonal for separator columns: X[j] = Y[j] + sum_{i>j} Linv[i][j] Y[i].
+// Lane per column (32-column tasks), rows i split over the warps, per-warp
+// partial sums combined in fixed warp order.
 __global__ void __launch_bounds__(256) k_bwd_diag(SolveArgs A, const Task* tasks) {
   extern __shared__ int s_mem[];
+  __shared__ cplx part[8][MR][32];
   const int c = blockIdx.y;
   const int m = load_members(A, c, s_mem);
   if (m == 0) return;
   const Task T = tasks[blockIdx.x];
   const DevSn sn = A.sn[T.s];
   const cplx* Linv = A.vals + (long long)c * A.nvals + sn.diag_off;
-  for (int j = T.a + threadIdx.x; j < T.b; j += blockDim.x) {
-    for (int mb = 0; mb < m; mb += MR) {
-      const int mc = min(MR, m - mb);
-      cplx acc[MR];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int j = T.a + lane;
+  const bool colok = j < T.b;
+  for (int mb = 0; mb < m; mb += MR) {
+    const int mc = min(MR, m - mb);
+    cplx acc[MR];
 #pragma unroll
-      for (int k = 0; k < MR; ++k) acc[k] = cmk(0, 0);
-      for (int i = j + 1; i < sn.n; ++i) {
+    for (int k = 0; k < MR; ++k) acc[k] = cmk(0, 0);
+    if (colok) {
+      for (int i = T.a + 1 + warp; i < sn.n; i += nwarp) {
+        if (i <= j) continue;
         const cplx l = ldg(Linv + (long long)i * (i - 1) / 2 + j);
 #pragma unroll
         for (int k = 0; k < MR; ++k)
           if (k < mc) cfma(acc[k], l, A.Y[(long long)s_mem[mb + k] * A.nw + sn.c0 + i]);
       }
+    }
 #pragma unroll
-      for (int k = 0; k < MR; ++k) {
-        if (k < mc) {
-          const long long p = (long long)s_mem[mb + k] * A.nw + sn.c0 + j;
-          A.X[p] = cadd(A.Y[p], acc[k]);
-        }
+    for (int k = 0; k < MR; ++k) part[warp][k][lane] = acc[k];
+    __syncthreads();
+    if (warp == 0 && colok) {
+      for (int k = 0; k < mc; ++k) {
+        cplx s = part[0][k][lane];
+        for (int w = 1; w < nwarp; ++w) s = cadd(s, part[w][k][lane]);
+        const long long p = (long long)s_mem[mb + k] * A.nw + sn.c0 + j;
+        A.X[p] = cadd(A.Y[p], s);
       }
     }
+    __syncthreads();
   }
 }
 
@@ -527,18 +621,15 @@ void launch_solve(const SolveArgs& A, const SolvePlan& P, int ncls, int max_memb
   }
   k_wprefix<<<1, 32, 0, st>>>(A.act_ptr, ncls, P.nsubtree, P.d_wprefix);
   launch_subtrees(A, P, ncls, max_rhs, true, st);
-  const size_t smem_pull =
-      ((sizeof(int) * size_t(max_members) + 15) & ~size_t(15)) + sizeof(int2) * 8 * P.seg_max_top;
   for (const auto& L : P.fwd) {
     dim3 g(L.ntask, ncls);
-    k_fwd_pull<<<g, 256, smem_pull, st>>>(A, L.d_tasks, P.seg_max_top, max_members);
+    k_fwd_pull<<<g, 256, smem, st>>>(A, L.d_tasks);
     k_fwd_diag<<<g, 256, smem, st>>>(A, L.d_tasks);
   }
   for (const auto& L : P.bwd) {
     dim3 g(L.ntask32, ncls);
     k_bwd_pull<<<g, 256, smem, st>>>(A, L.d_tasks32);
-    dim3 g2(L.ntask, ncls);
-    k_bwd_diag<<<g2, 256, smem, st>>>(A, L.d_tasks);
+    k_bwd_diag<<<g, 256, smem, st>>>(A, L.d_tasks32);
   }
   launch_subtrees(A, P, ncls, max_rhs, false, st);
 }

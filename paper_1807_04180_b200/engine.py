@@ -140,6 +140,7 @@ def load_library(path: str = LIB_PATH):
         "hddm_window_dims": (C.c_int, [vp, ip, ip]),
         "hddm_nd_order": (C.c_int, [C.c_int, C.c_int, ip]),
         "hddm_footprint": (C.c_int, [vp, P(C.c_long), P(C.c_long), P(C.c_long)]),
+        "hddm_symbolic_stats": (C.c_int, [C.c_int, C.c_int, P(C.c_long), P(C.c_long), ip, ip]),
         "hddm_set_timing": (C.c_int, [vp, C.c_int]),
         "hddm_stage_times": (C.c_int, [vp, dp, P(C.c_longlong), C.c_int, ip]),
         "hddm_launch_count": (C.c_longlong, [vp]),
@@ -172,6 +173,16 @@ def nd_order(nx: int, ny: int) -> np.ndarray:
     out = np.zeros(nx * ny, np.int32)
     lib.hddm_nd_order(nx, ny, out.ctypes.data_as(C.POINTER(C.c_int)))
     return out
+
+
+def symbolic_stats(nx: int, ny: int) -> dict:
+    """Host-only symbolic analysis (no GPU): reference nnz, stored entries."""
+    lib = load_library()
+    a, b, c, d = C.c_long(), C.c_long(), C.c_int(), C.c_int()
+    rc = lib.hddm_symbolic_stats(nx, ny, C.byref(a), C.byref(b), C.byref(c), C.byref(d))
+    if rc:
+        _raise(rc, lib.hddm_last_error(None).decode())
+    return dict(nnz_ref=a.value, stored=b.value, supernodes=c.value, height=d.value)
 
 
 class DdmEngine:

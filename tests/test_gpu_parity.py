@@ -1,0 +1,159 @@
+"""CUDA engine vs the reference (golden fixtures) and the C restatement on
+identical inputs, through the C-ABI. Tolerances (BASELINE.json north_star):
+per-iteration iterate rel-L2 <= 1e-10, final solution <= 1e-8, identical
+iteration / solve / skip counts."""
+import numpy as np
+import pytest
+
+import pyoracle
+from conftest import golden, golden_cases, rel_l2
+
+pytestmark = pytest.mark.gpu
+CASES = golden_cases()
+ITER_TOL = 1e-10
+FINAL_TOL = 1e-8
+
+
+@pytest.fixture(scope="module")
+def engines():
+    from paper_1807_04180_b200.engine import DdmEngine
+    cache = {}
+
+    def get(prob):
+        if prob.name not in cache:
+            cache[prob.name] = DdmEngine(prob)
+        return cache[prob.name]
+    yield get
+    for e in cache.values():
+        e.close()
+
+
+@pytest.mark.parametrize("name,prob,run", CASES, ids=[c[0] for c in CASES])
+def test_setup_matches_reference(engines, name, prob, run):
+    g = golden(name)
+    e = engines(prob)
+    ci = e.class_info()
+    assert [c["members"] for c in ci] == g["members"].tolist()
+    assert [c["factor_nnz"] for c in ci] == g["factor_nnz"].tolist()
+    assert all(c["backend"] == "ldlt" and c["probe_relres"] <= 1e-10 for c in ci)
+    assert abs(e.sigma0() - float(g["sigma0"])) <= 1e-14 * float(g["sigma0"])
+
+
+@pytest.mark.parametrize("name,prob,run", CASES, ids=[c[0] for c in CASES])
+def test_standalone_iterates_match_reference(engines, name, prob, run):
+    from paper_1807_04180_b200.engine import DdmStats
+    g = golden(name)
+    e = engines(prob)
+    f = prob.source_f()
+    st = DdmStats()
+    u = e.solve_iterative(f, 0.0, run["steps"], st)
+    assert rel_l2(u, g["u_steps"]) <= ITER_TOL
+    assert (st.steps, st.solves, st.skipped) == (int(g["steps"]), int(g["solves"]),
+                                                 int(g["skipped"]))
+    assert [h.step for h in st.history] == list(range(1, run["steps"] + 1))
+    np.testing.assert_allclose([h.relres for h in st.history], g["relres_hist"], rtol=1e-6, atol=1e-10)
+    if g["per_step"].size:
+        for s in range(run["steps"]):
+            z = e.precondition(f, s + 1)
+            assert rel_l2(z, g["per_step"][s]) <= ITER_TOL, s
+
+
+@pytest.mark.parametrize("name,prob,run", [c for c in CASES if "fgmres" in c[2]],
+                         ids=[c[0] for c in CASES if "fgmres" in c[2]])
+def test_fgmres_matches_reference(engines, name, prob, run):
+    from paper_1807_04180_b200.engine import DdmStats, FgmresOptions
+    g = golden(name)
+    e = engines(prob)
+    fg = run["fgmres"]
+    ps = DdmStats()
+    x, res = e.fgmres(prob.source_f(), FgmresOptions(fg["tol"], fg["max_iters"], fg["restart"]),
+                      fg["K"], ps)
+    assert res.iters == int(g["fg_iters"]) and res.converged
+    assert rel_l2(x, g["fg_x"]) <= FINAL_TOL
+    np.testing.assert_allclose(res.history, g["fg_hist"], rtol=1e-6, atol=1e-10)
+    assert (ps.solves, ps.skipped) == (int(g["fg_solves"]), int(g["fg_skipped"]))
+    assert abs(res.true_relres - float(g["fg_true"])) <= 1e-6 * float(g["fg_true"]) + 1e-10
+
+
+@pytest.mark.parametrize("name,prob,run", CASES[:2], ids=[c[0] for c in CASES[:2]])
+def test_apply_global_matches_reference(engines, name, prob, run):
+    g = golden(name)
+    e = engines(prob)
+    assert rel_l2(e.apply_global(g["apply_in"]), g["apply_out"]) <= 1e-14
+
+
+def test_local_class_solves_match_oracle(engines):
+    """Batched supernodal solve vs the restatement's Factorization::solve."""
+    from paper_1807_04180_b200.problems import config
+    prob = config(1)
+    e = engines(prob)
+    o = pyoracle.OracleEngine(prob)
+    nx, ny = e.window_dims()
+    rng = np.random.default_rng(11)
+    for c in range(len(e.class_info())):
+        b = rng.standard_normal(nx * ny) + 1j * rng.standard_normal(nx * ny)
+        xg, rg = e.class_solve(c, b)
+        xo, ro = o.class_solve(c, b)
+        assert rel_l2(xg, xo) <= 1e-12
+        assert rg <= 1e-11
+
+
+def test_subdomain_taps_match_oracle(engines):
+    """Per-subdomain right-hand sides (gather-sources kernels) and local
+    solutions after a step, against the restatement."""
+    from paper_1807_04180_b200.problems import small
+    prob = small(80, 2, 2, 8.0, 10, 20, source=("gaussian", 0.41, 0.63, 0.02))
+    e = engines(prob)
+    o = pyoracle.OracleEngine(prob)
+    f = prob.source_f()
+    for K in (1, 2, 3):
+        e.precondition(f, K)
+        o.precondition(f, K)
+        taps = [(e.tap_subdomain(t), o.tap_subdomain(t)) for t in range(prob.nsub)]
+        # subdomains whose incoming sources are still rounding-level (cancellation
+        # in L_t(beta v) where the taper is flat) are compared on the scale of
+        # the largest local solution of the step
+        scale_r = max(np.linalg.norm(ro) for (_, (ro, _, _)) in taps)
+        scale_u = max(np.linalg.norm(uo) for (_, (_, uo, _)) in taps)
+        for (rg, ug, ag), (ro, uo, ao) in taps:
+            assert ag == ao
+            if ag:
+                assert np.linalg.norm(rg - ro) <= 1e-7 * scale_r
+                assert np.linalg.norm(ug - uo) <= ITER_TOL * scale_u
+
+
+def test_lens_medium_matches_oracle():
+    """BASELINE config 3's medium kind (reference extension), small grid."""
+    from paper_1807_04180_b200.engine import DdmEngine, DdmStats
+    from paper_1807_04180_b200.problems import MEDIUM_LENS, small
+    prob = small(64, 4, 4, 6.0, 4, 8, source=("gaussian", 0.25, 0.25, 0.02)).with_(
+        medium_kind=MEDIUM_LENS, lens=(0.4, 0.5, 0.5, 0.05))
+    e = DdmEngine(prob)
+    o = pyoracle.OracleEngine(prob)
+    assert [c["members"] for c in e.class_info()] == [c["members"] for c in o.class_info()]
+    f = prob.source_f()
+    st = DdmStats()
+    u = e.solve_iterative(f, 0.0, 6, st)
+    uo, so = o.solve_iterative(f, 0.0, 6)
+    assert rel_l2(u, uo) <= ITER_TOL and (st.solves, st.skipped) == (so.solves, so.skipped)
+    e.close()
+
+
+def test_cfg2_fgmres_matches_oracle():
+    """BASELINE config 2 end to end (1024^2, 8x8, FGMRES(30)+DDM(K=16)) against
+    the C restatement (pinned bit-for-bit to the reference by test_oracle)."""
+    from paper_1807_04180_b200.engine import DdmEngine, DdmStats, FgmresOptions
+    from paper_1807_04180_b200.problems import config
+    prob = config(2)
+    e = DdmEngine(prob)
+    o = pyoracle.OracleEngine(prob)
+    f = prob.source_f()
+    ps = DdmStats()
+    x, res = e.fgmres(f, FgmresOptions(prob.tol, prob.max_iters, prob.restart), prob.k_steps, ps)
+    xo, ro, pso, zo = o.fgmres(f, prob.tol, prob.max_iters, prob.restart, prob.k_steps, keep_z=1)
+    assert res.iters == ro.iters and res.converged == ro.converged
+    assert rel_l2(x, xo) <= FINAL_TOL
+    assert (ps.solves, ps.skipped) == (pso.solves, pso.skipped)
+    z = e.precondition(f / np.linalg.norm(f), prob.k_steps)
+    assert rel_l2(z, zo[0]) <= ITER_TOL
+    e.close()

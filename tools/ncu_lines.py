@@ -1,0 +1,77 @@
+"""Attribute ncu warp-stall samples (SASS source page) to CUDA source lines.
+
+usage: ncu_lines.py REPORT.ncu-rep KERNEL_REGEX LIB.so FUNC_SUBSTR [top]
+Extracts the cubins from LIB.so, maps SASS offsets to lines with `nvdisasm -g`,
+and sums the samples of the profiled kernel per source line."""
+import collections
+import csv
+import glob
+import os
+import re
+import subprocess
+import sys
+import tempfile
+
+
+def line_map(lib, func_sub):
+    tmp = tempfile.mkdtemp()
+    subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp,
+                   stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+    for cub in glob.glob(os.path.join(tmp, "*.cubin")):
+        txt = subprocess.run(["nvdisasm", "-g", "-c", cub], capture_output=True, text=True).stdout
+        m = None
+        for sec in txt.split("//--------------------- .text."):
+            if sec.startswith(func_sub) or func_sub in sec.split(" ")[0]:
+                m = sec
+                break
+        if m is None:
+            continue
+        cur = None
+        out = {}
+        for ln in m.splitlines():
+            g = re.search(r'line (\d+)', ln) if "//## File" in ln else None
+            if g:
+                cur = int(g.group(1))
+                continue
+            a = re.search(r'/\*([0-9a-f]{4,})\*/', ln)
+            if a and cur is not None:
+                out[int(a.group(1), 16)] = cur
+        return out
+    raise SystemExit("function not found")
+
+
+def samples(rep, kregex):
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
+                          "-k", f"regex:{kregex}"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(txt.splitlines()))
+    hdr = None
+    out = []
+    for r in rows:
+        if r and r[0] == "Address":
+            if hdr is not None:
+                break  # first kernel only
+            hdr = {k: i for i, k in enumerate(r)}
+            continue
+        if hdr and len(r) >= len(hdr):
+            out.append((int(r[hdr["Address"]], 16), float(r[hdr["Warp Stall Sampling (All Samples)"]] or 0)))
+    base = min(a for a, _ in out)
+    return [(a - base, s) for a, s in out]
+
+
+def main():
+    rep, kre, lib, fsub = sys.argv[1:5]
+    top = int(sys.argv[5]) if len(sys.argv) > 5 else 25
+    lm = line_map(lib, fsub)
+    src = open(os.path.join(os.path.dirname(lib), "csrc", "kernels_solve.cu")).read().splitlines() \
+        if os.path.exists(os.path.join(os.path.dirname(lib), "csrc", "kernels_solve.cu")) else []
+    acc = collections.Counter()
+    for off, s in samples(rep, kre):
+        acc[lm.get(off, -1)] += s
+    tot = sum(acc.values())
+    for ln, s in acc.most_common(top):
+        text = src[ln - 1].strip()[:90] if 0 < ln <= len(src) else ""
+        print(f"{100 * s / tot:5.1f}%  L{ln:<5d} {text}")
+
+
+if __name__ == "__main__":
+    main()
