@@ -162,6 +162,16 @@ int hddm_set_timing(hddm_engine* e, int enable);
 int hddm_stage_times(hddm_engine* e, double* ms, long long* count, int cap, int* n);
 const char* hddm_stage_name(int i);
 long long hddm_launch_count(const hddm_engine* e);
+/* Device time of one batched solve stage (forward + backward sweeps of every
+ * class for all subdomains, steady state: all active), averaged over reps
+ * CUDA-graph launches on the engine stream; uses the right-hand sides of the
+ * last sweep. hddm_solve_launches: kernels in that stage. */
+int hddm_time_solve(hddm_engine* e, int reps, double* ms_per_solve);
+int hddm_solve_launches(const hddm_engine* e);
+/* Refinement diagnostics of the last call: the largest local-solve residual
+ * ||b - A x||/||b|| seen (refine's first pass, sparse.cpp:268-292) and how many
+ * local solves exceeded the reference's 1e-11 correction threshold. */
+int hddm_refine_stats(const hddm_engine* e, double* max_local_relres, int* corrections);
 /* CUDA stream (cudaStream_t) the engine orders its work on. */
 void* hddm_stream(const hddm_engine* e);
 

@@ -43,6 +43,9 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 __device__ __forceinline__ cplx ldg(const cplx* p) { return __ldg(p); }
+// factor entries are streamed once per pass: evict-first in L1/L2 so the
+// per-subdomain vectors (reused across levels) stay cached
+__device__ __forceinline__ cplx ldf(const cplx* p) { return __ldcs(p); }
 
 // Asynchronous bulk prefetch of a contiguous global range into L2 (TMA path,
 // sm_90+). p must be 16-byte aligned and bytes a multiple of 16.

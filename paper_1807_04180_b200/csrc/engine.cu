@@ -73,6 +73,8 @@ struct hddm_engine {
   size_t dev_bytes = 0;
   std::vector<void*> allocs;
   int last_step = 0;
+  double last_max_rel = 0;
+  int last_refine_count = 0;
   bool timing = false;
   double stage_ms[kStages] = {};
 
@@ -112,6 +114,20 @@ struct hddm_engine {
   double* d_rel = nullptr;
   int* d_refine = nullptr;
   double* d_maxrel = nullptr;
+  // device refinement state (refine, sparse.cpp:268-292)
+  cplx* d_R = nullptr;
+  cplx* d_C = nullptr;
+  double* d_relcur = nullptr;
+  int* d_need = nullptr;
+  int* d_ncorr = nullptr;
+  int* d_undo = nullptr;
+  int* d_any = nullptr;
+  long long* d_nfix = nullptr;
+  // one CUDA graph per step variant (step 1; s >= 2 by s mod 3), each with a
+  // conditional WHILE node running the refinement corrections on demand
+  cudaStream_t st2 = nullptr;
+  cudaGraphExec_t step_exec[4] = {};
+  int step_kernels = 0;
   // global
   cplx* d_ga = nullptr;
   double* d_k2 = nullptr;
@@ -165,6 +181,9 @@ struct hddm_engine {
     for (void* p : allocs) cudaFree(p);
     for (auto& e : ev_pool) cudaEventDestroy(e);
     if (h_scal) cudaFreeHost(h_scal);
+    for (auto& g : step_exec)
+      if (g) cudaGraphExecDestroy(g);
+    if (st2) cudaStreamDestroy(st2);
     if (st) cudaStreamDestroy(st);
   }
 
@@ -173,7 +192,13 @@ struct hddm_engine {
   void run_probe();
   StepArgs step_args(int s, const cplx* f);
   SolveArgs solve_args(const cplx* B, cplx* X, cplx* Y);
-  void enqueue_step(int s, const cplx* f);
+  CheckArgs check_args(const cplx* Bp, const cplx* X, const int* zc, const int* only);
+  RefineArgs refine_args(const cplx* Bp, cplx* X, const int* zc, unsigned long long cond);
+  void enqueue_step_front(int s, cudaStream_t stream, unsigned long long cond);
+  void enqueue_refine_body(int s, cudaStream_t stream, unsigned long long cond);
+  void build_step_graph(int v);
+  void run_step(int s);
+  void host_refine(const cplx* Bp, cplx* X, const int* zc);
   void reset_state();
   void fill_flags(int* p, int v, int n);
   double device_norm(const cplx* v);
@@ -238,6 +263,7 @@ void hddm_engine::create(const hddm_problem& p) {
   if (dev < 0 || dev >= ndev) throw ConfigErr("invalid CUDA device ordinal");
   CK(cudaSetDevice(dev));
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
   CK(cudaMallocHost(&h_scal, 64 * sizeof(double)));
   nsub = S.n1 * S.n2;
   ncls = S.ncls;
@@ -380,6 +406,15 @@ void hddm_engine::create(const hddm_problem& p) {
   d_rel = dalloc<double>(nsub);
   d_refine = dalloc<int>(1);
   d_maxrel = dalloc<double>(1);
+  d_R = dalloc<cplx>(size_t(nsub) * nw);
+  d_C = dalloc<cplx>(size_t(nsub) * nw);
+  d_relcur = dalloc<double>(nsub);
+  d_need = dalloc<int>(nsub);
+  d_ncorr = dalloc<int>(nsub);
+  d_undo = dalloc<int>(nsub);
+  d_any = dalloc<int>(1);
+  d_nfix = dalloc<long long>(1);
+  CK(cudaMemsetAsync(d_nfix, 0, sizeof(long long), st));
 
   // ---- global data
   std::vector<cplx> ga(size_t(2) * S.gnx + 2 * S.gny);
@@ -460,123 +495,51 @@ void hddm_engine::create(const hddm_problem& p) {
 
   factorize();
   run_probe();
-  // profiling knob: skip subtree phase kinds in DDM steps (results invalid)
-  if (const char* dbg = std::getenv("HDDM_DEBUG_SKIP")) plan.sub.dbg = std::atoi(dbg);
 }
 
-// Solve plan: maximal subtrees of at most kSubtreeMax nodes run as one CTA each
-// (vectors in shared memory); the separators above them run level by level.
+// Solve plan: the ND tree level by level. Forward: leaves, then separator rows
+// by height; backward: separator columns by depth, then leaf columns, then the
+// leaves' band back-substitution.
 void hddm_engine::build_plan() {
-  constexpr int kSubtreeMax = 600;
   const int nsn = int(Y.sn.size());
-  std::vector<int> size(nsn, 0), cnt(nsn, 0);
-  for (int s = 0; s < nsn; ++s) {  // postorder: children first
-    size[s] = Y.sn[s].n;
-    cnt[s] = 1;
-    for (int k = 0; k < Y.sn[s].nch; ++k) {
-      size[s] += size[Y.sn[s].child[k]];
-      cnt[s] += cnt[Y.sn[s].child[k]];
+  std::vector<int2> leaves, leafcols;
+  for (int s = 0; s < nsn; ++s)
+    if (Y.sn[s].kind == 0) {
+      leaves.push_back(make_int2(s, 0));
+      for (int j = 0; j < Y.sn[s].n; ++j) leafcols.push_back(make_int2(s, j));
     }
-  }
-  std::vector<int> root_of(nsn, -1);
-  std::vector<int> roots;
-  for (int s = nsn - 1; s >= 0; --s) {  // parents before children
-    const int p = Y.sn[s].parent;
-    if (p >= 0 && root_of[p] >= 0) {
-      root_of[s] = root_of[p];
-    } else if (size[s] <= kSubtreeMax) {
-      root_of[s] = s;
-      roots.push_back(s);
-    }
-  }
-  std::sort(roots.begin(), roots.end());
-  std::vector<SubtreeInfo> st;
-  std::vector<Phase> ph;
-  std::vector<int2> items;
-  int np_max = 1, items_max = 1;
-  for (int r : roots) {
-    SubtreeInfo I;
-    I.np = size[r];
-    I.p0 = Y.sn[r].c0 + Y.sn[r].n - size[r];
-    I.ph0 = int(ph.size());
-    const int hmax = Y.sn[r].height;
-    for (int h = 0; h <= hmax; ++h) {
-      Phase P{};
-      P.kind = h == 0 ? 0 : 1;
-      P.it0 = int(items.size());
-      for (int s = r - cnt[r] + 1; s <= r; ++s) {
-        // supernodes of the subtree are a contiguous postorder index range
-        if (root_of[s] != r || Y.sn[s].height != h) continue;
-        if (h == 0)
-          items.push_back(make_int2(s, 0));
-        else
-          for (int i = 0; i < Y.sn[s].n; ++i) items.push_back(make_int2(s, i));
-      }
-      P.nit = int(items.size()) - P.it0;
-      if (P.nit == 0) continue;
-      items_max = std::max(items_max, P.nit);
-      if (h == 0) {  // leaf columns for the backward block products
-        P.ic0 = int(items.size());
-        for (int q = P.it0; q < P.it0 + P.nit; ++q)
-          for (int j = 0; j < Y.sn[items[q].x].n; ++j) items.push_back(make_int2(items[q].x, j));
-        P.nic = int(items.size()) - P.ic0;
-      }
-      ph.push_back(P);
-    }
-    I.nph = int(ph.size()) - I.ph0;
-    np_max = std::max(np_max, I.np);
-    st.push_back(I);
-  }
-  // sanity: a subtree's supernodes are the postorder index range [r-cnt+1, r]
-  for (int r : roots)
-    for (int s = r - cnt[r] + 1; s <= r; ++s)
-      if (root_of[s] != r) throw std::runtime_error("subtree is not contiguous in postorder");
-  plan.nsubtree = int(st.size());
-  plan.d_wprefix = dalloc<int>(ncls + 1);
-  plan.sub.st = upload(st);
-  plan.sub.ph = upload(ph);
-  plan.sub.items = upload(items);
-  plan.sub.np_max = np_max;
-  plan.sub.items_max = items_max;
-  // top separators: forward by height, backward by depth
-  const int R = 8, C = 256;
-  for (int h = 1; h <= Y.max_height; ++h) {
-    std::vector<Task> t;
-    for (int s = 0; s < nsn; ++s)
-      if (root_of[s] < 0 && Y.sn[s].height == h)
-        for (int a = 0; a < Y.sn[s].n; a += R) t.push_back({s, a, std::min(a + R, Y.sn[s].n), 0});
-    if (t.empty()) continue;
+  auto level = [&](const std::vector<int2>& v) {
     SolveLevel L;
-    L.ntask = int(t.size());
-    L.d_tasks = upload(t);
+    L.nitem = int(v.size());
+    L.d_items = upload(v);
+    return L;
+  };
+  for (const SnNode& nd : Y.sn)  // register-window bound of the leaf band kernels
+    if (nd.kind == 0)
+      for (int i = 0; i < nd.n; ++i)
+        if (i - Y.row_first[nd.drow0 + i] > 6) throw std::runtime_error("leaf band wider than 6");
+  plan.fwd_leaf = level(leaves);
+  plan.bwd_leaf = level(leaves);
+  plan.bwd_leafcol = level(leafcols);
+  for (int h = 1; h <= Y.max_height; ++h) {
+    std::vector<int2> v;
+    for (int s = 0; s < nsn; ++s)
+      if (Y.sn[s].kind == 1 && Y.sn[s].height == h)
+        for (int i = 0; i < Y.sn[s].n; ++i) v.push_back(make_int2(s, i));
+    if (v.empty()) continue;
+    SolveLevel L = level(v);
+    long tot = 0;
+    for (const int2& it : v) tot += Y.run_off[Y.sn[it.x].c0 + it.y + 1] - Y.run_off[Y.sn[it.x].c0 + it.y];
+    L.warp_rows = tot > 128L * long(v.size());  // average run longer than 4 warp strides
     plan.fwd.push_back(L);
   }
   for (int d = 0; d <= Y.max_depth; ++d) {
-    std::vector<Task> t, t32;
+    std::vector<int2> v;
     for (int s = 0; s < nsn; ++s)
-      if (root_of[s] < 0 && Y.sn[s].depth == d) {
-        if (Y.sn[s].kind == 0) throw std::runtime_error("leaf above the subtree cut");
-        for (int a = 0; a < Y.sn[s].n; a += C) t.push_back({s, a, std::min(a + C, Y.sn[s].n), 0});
-        for (int a = 0; a < Y.sn[s].n; a += 32) t32.push_back({s, a, std::min(a + 32, Y.sn[s].n), 0});
-      }
-    if (t.empty()) continue;
-    SolveLevel L;
-    L.ntask = int(t.size());
-    L.d_tasks = upload(t);
-    L.ntask32 = int(t32.size());
-    L.d_tasks32 = upload(t32);
-    plan.bwd.push_back(L);
+      if (Y.sn[s].kind == 1 && Y.sn[s].depth == d)
+        for (int i = 0; i < Y.sn[s].n; ++i) v.push_back(make_int2(s, i));
+    if (!v.empty()) plan.bwd.push_back(level(v));
   }
-  // segment-table bounds (per-warp shared scratch of the row pulls)
-  int seg_sub = 1, seg_top = 1;
-  for (int p = 0; p < Y.n; ++p) {
-    const int ns = Y.seg_ptr[p + 1] - Y.seg_ptr[p];
-    const int sn = Y.sn_of_pos[p];
-    if (sn < 0) continue;
-    if (root_of[sn] >= 0) seg_sub = std::max(seg_sub, ns); else seg_top = std::max(seg_top, ns);
-  }
-  plan.sub.seg_max = seg_sub;
-  plan.seg_max_top = seg_top;
 }
 
 // ----------------------------------------------------------------- factorization
@@ -719,35 +682,13 @@ void hddm_engine::run_probe() {
   CK(cudaMemcpyAsync(d_act_ptr, aptr.data(), sizeof(int) * (ncls + 1), cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_act_list, alist.data(), sizeof(int) * ncls, cudaMemcpyHostToDevice, st));
   CK(cudaStreamSynchronize(st));
-  launch_solve(solve_args(d_B, d_U[0], d_Y), plan, ncls, 1, ncls, st);
-  CheckArgs C;
-  C.nw = nw;
-  C.wnx = wnx;
-  C.wny = wny;
-  C.gnx = S.gnx;
-  C.nring = Y.nring;
-  C.ih2 = 1.0 / (S.h * S.h);
-  C.sub = d_sub;
-  C.sa = d_sa;
-  C.sa_stride = sa_stride;
-  C.k2 = d_k2;
-  C.perm = d_perm;
-  C.pinv = d_pinv;
-  C.zc = d_Z[0];
-  C.nsub = nsub;
-  C.B = d_B;
-  C.X = d_U[0];
-  C.part = d_part_chk;
-  C.nchunk = nchunk;
-  C.rel = d_rel;
-  C.refine_flag = d_refine;
-  C.max_rel = d_maxrel;
+  launch_solve(solve_args(d_B, d_U[0], d_Y), plan, ncls, ncls, st);
   CK(cudaMemsetAsync(d_refine, 0, sizeof(int), st));
   CK(cudaMemsetAsync(d_maxrel, 0, sizeof(double), st));
-  launch_check(C, st);
+  host_refine(d_B, d_U[0], d_Z[0]);
   CK(cudaGetLastError());
   std::vector<double> rel(nsub);
-  CK(cudaMemcpyAsync(rel.data(), d_rel, sizeof(double) * nsub, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(rel.data(), d_relcur, sizeof(double) * nsub, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   probe.assign(ncls, 0);
   for (int c = 0; c < ncls; ++c) {
@@ -821,48 +762,157 @@ void hddm_engine::reset_state() {
   last_step = 0;
 }
 
-// one DDM iteration, DdmEngine::sweep (ddm.cpp:174-214)
-void hddm_engine::enqueue_step(int s, const cplx* f) {
-  const StepArgs A = step_args(s, f);
-  stage_begin(0);
-  launch_flags(A, ncls, st);
-  launch_gather(A, st);
-  stage_end(0);
-  stage_begin(1);
-  launch_solve(solve_args(d_B, A.Ucur, d_Y), plan, ncls, max_members, nsub, st);
-  stage_end(1);
-  stage_begin(2);
+CheckArgs hddm_engine::check_args(const cplx* Bp, const cplx* X, const int* zc,
+                                  const int* only) {
   CheckArgs C;
   C.nw = nw;
   C.wnx = wnx;
   C.wny = wny;
   C.gnx = S.gnx;
   C.nring = Y.nring;
-  C.ih2 = A.ih2;
+  C.ih2 = 1.0 / (S.h * S.h);
   C.sub = d_sub;
   C.sa = d_sa;
   C.sa_stride = sa_stride;
   C.k2 = d_k2;
   C.perm = d_perm;
   C.pinv = d_pinv;
-  C.zc = A.zc;
+  C.zc = zc;
+  C.only = only;
   C.nsub = nsub;
-  C.B = d_B;
-  C.X = A.Ucur;
+  C.B = Bp;
+  C.X = X;
   C.part = d_part_chk;
   C.nchunk = nchunk;
   C.rel = d_rel;
   C.refine_flag = d_refine;
   C.max_rel = d_maxrel;
-  launch_check(C, st);
-  stage_end(2);
-  stage_begin(3);
-  launch_accumulate(A, st);
-  stage_end(3);
-  launches += 3 + solve_launches() + 2 + 1;
-  // bound the pending event list inside long runs
-  if (timing && ev_next > 4096) stage_resolve();
+  return C;
+}
+
+RefineArgs hddm_engine::refine_args(const cplx* Bp, cplx* X, const int* zc,
+                                    unsigned long long cond) {
+  RefineArgs R;
+  R.nsub = nsub;
+  R.ncls = ncls;
+  R.nw = nw;
+  R.wnx = wnx;
+  R.wny = wny;
+  R.gnx = S.gnx;
+  R.nchunk = nchunk;
+  R.ih2 = 1.0 / (S.h * S.h);
+  R.sub = d_sub;
+  R.sa = d_sa;
+  R.sa_stride = sa_stride;
+  R.k2 = d_k2;
+  R.perm = d_perm;
+  R.pinv = d_pinv;
+  R.zc = zc;
+  R.B = Bp;
+  R.X = X;
+  R.R = d_R;
+  R.C = d_C;
+  R.part = d_part_chk;
+  R.rel_cur = d_relcur;
+  R.need = d_need;
+  R.ncorr = d_ncorr;
+  R.undo = d_undo;
+  R.any = d_any;
+  R.nfix = d_nfix;
+  R.cls_ptr = d_cls_ptr;
+  R.cls_mem = d_cls_mem;
+  R.act_ptr = d_act_ptr;
+  R.act_list = d_act_list;
+  R.cond = cond;
+  return R;
+}
+
+// One DDM iteration, DdmEngine::sweep (ddm.cpp:174-214), up to the first
+// refine pass: flags -> RHS assembly -> batched solves -> residual check.
+void hddm_engine::enqueue_step_front(int s, cudaStream_t stream, unsigned long long cond) {
+  const StepArgs A = step_args(s, d_f);
+  launch_flags(A, ncls, stream);
+  launch_gather(A, stream);
+  launch_solve(solve_args(d_B, A.Ucur, d_Y), plan, ncls, nsub, stream);
+  launch_check(check_args(d_B, A.Ucur, A.zc, nullptr), stream);
+  launch_refine_init(refine_args(d_B, A.Ucur, A.zc, cond), stream);
+}
+
+// One correction pass of refine for every RHS still above 1e-11.
+void hddm_engine::enqueue_refine_body(int s, cudaStream_t stream, unsigned long long cond) {
+  const StepArgs A = step_args(s, d_f);
+  const RefineArgs R = refine_args(d_B, A.Ucur, A.zc, cond);
+  launch_refine_prep(R, stream);
+  launch_solve(solve_args(d_R, d_C, d_Y), plan, ncls, nsub, stream);
+  launch_refine_apply(R, stream);
+  launch_check_partials(check_args(d_B, A.Ucur, A.zc, d_need), stream);
+  launch_refine_decide(R, stream);
+  launch_refine_undo(R, stream);
+}
+
+static int variant_of(int s) { return s == 1 ? 0 : 1 + (s % 3); }
+static int rep_step(int v) { return v == 0 ? 1 : (v == 1 ? 3 : (v == 2 ? 4 : 2)); }
+
+void hddm_engine::build_step_graph(int v) {
+  const int s = rep_step(v);
+  cudaGraph_t g;
+  CK(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
+  CK(cudaStreamBeginCaptureToGraph(st, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  enqueue_step_front(s, st, (unsigned long long)h);
+  cudaStreamCaptureStatus cs;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &deps, &nd));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t wn;
+  CK(cudaGraphAddNode(&wn, g, deps, nd, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CK(cudaStreamUpdateCaptureDependencies(st, &wn, 1, cudaStreamSetCaptureDependencies));
+  CK(cudaStreamBeginCaptureToGraph(st2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  enqueue_refine_body(s, st2, (unsigned long long)h);
+  cudaGraph_t bout;
+  CK(cudaStreamEndCapture(st2, &bout));
+  launch_accumulate(step_args(s, d_f), st);
+  cudaGraph_t gout;
+  CK(cudaStreamEndCapture(st, &gout));
+  CK(cudaGraphInstantiate(&step_exec[v], g, 0));
+  CK(cudaGraphDestroy(g));
+  // kernels per step when no correction runs: flags, 2 RHS, solve, check (2),
+  // refine init, accumulate
+  step_kernels = 1 + 2 + solve_launches() + 2 + 1 + 1;
+}
+
+void hddm_engine::run_step(int s) {
+  const int v = variant_of(s);
+  if (!step_exec[v]) build_step_graph(v);
+  CK(cudaGraphLaunch(step_exec[v], st));
+  launches += step_kernels;
   last_step = s;
+}
+
+// Host-driven refinement (setup-time probe and class-solve taps).
+void hddm_engine::host_refine(const cplx* Bp, cplx* X, const int* zc) {
+  launch_check(check_args(Bp, X, zc, nullptr), st);
+  const RefineArgs R = refine_args(Bp, X, zc, 0);
+  launch_refine_init(R, st);
+  for (int it = 0; it < 13; ++it) {
+    int any = 0;
+    CK(cudaMemcpyAsync(&any, d_any, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (!any) break;
+    launch_refine_prep(R, st);
+    launch_solve(solve_args(d_R, d_C, d_Y), plan, ncls, nsub, st);
+    launch_refine_apply(R, st);
+    launch_check_partials(check_args(Bp, X, zc, d_need), st);
+    launch_refine_decide(R, st);
+    launch_refine_undo(R, st);
+  }
 }
 
 double hddm_engine::device_norm(const cplx* v) {
@@ -942,11 +992,14 @@ void read_counts(hddm_engine* e, long long* c) {
 }
 
 void check_refine(hddm_engine* e) {
-  if (e->plan.sub.dbg) return;  // profiling knob active: results are invalid by design
   int flag = 0;
+  double mx = 0;
   CK(cudaMemcpyAsync(&flag, e->d_refine, sizeof(int), cudaMemcpyDeviceToHost, e->st));
+  CK(cudaMemcpyAsync(&mx, e->d_maxrel, sizeof(double), cudaMemcpyDeviceToHost, e->st));
   CK(cudaStreamSynchronize(e->st));
-  if (flag)
+  e->last_max_rel = mx;
+  e->last_refine_count = flag;  // solves whose first pass exceeded 1e-11 (corrected on device)
+  if (false)
     throw SolveErr(
         "a local solve needed iterative-refinement corrections (relres > 1e-11); "
         "correction passes are not implemented on the GPU path");
@@ -1041,6 +1094,9 @@ int hddm_solve_iterative(hddm_engine* e, const double* f, double tol, int max_st
     st.relres = -1;
     st.factor_ms = e->factor_ms;
     const cplx* df = in_ptr(e, f, memkind, e->d_f);
+    if (df != e->d_f)
+      CK(cudaMemcpyAsync(e->d_f, df, e->ng * sizeof(cplx), cudaMemcpyDeviceToDevice, e->st));
+    df = e->d_f;
     const double bnorm = e->device_norm(df);
     int nh = 0;
     e->reset_state();
@@ -1056,7 +1112,7 @@ int hddm_solve_iterative(hddm_engine* e, const double* f, double tol, int max_st
       GlobalArgs G{e->S.gnx, e->S.gny, 1.0 / (e->S.h * e->S.h), e->d_ga, e->d_k2};
       for (int s = 1; s <= max_steps; ++s) {
         const double t0 = now_ms();
-        e->enqueue_step(s, df);
+        e->run_step(s);
         st.steps = s;
         if (s % check_every == 0 || s == max_steps) {
           // residual_norm, ddm.cpp:237-242
@@ -1098,14 +1154,18 @@ int hddm_precondition(hddm_engine* e, const double* r, double* z, int ksteps, in
                       hddm_stats* stats) {
   return guarded(e, [&] {
     const cplx* dr = in_ptr(e, r, memkind, e->d_f);
+    if (dr != e->d_f)
+      CK(cudaMemcpyAsync(e->d_f, dr, e->ng * sizeof(cplx), cudaMemcpyDeviceToDevice, e->st));
+    dr = e->d_f;
     const double t0 = now_ms();
     e->reset_state();
     CK(cudaMemsetAsync(e->d_counts, 0, 2 * sizeof(long long), e->st));
     CK(cudaMemsetAsync(e->d_refine, 0, sizeof(int), e->st));
+    CK(cudaMemsetAsync(e->d_maxrel, 0, sizeof(double), e->st));
     StepArgs A0 = e->step_args(1, dr);
     launch_fany(A0, e->st);
     e->launches += 4;  // 3 flag fills + fany
-    for (int s = 1; s <= ksteps; ++s) e->enqueue_step(s, dr);
+    for (int s = 1; s <= ksteps; ++s) e->run_step(s);
     out_copy(e, z, e->d_asm, memkind);
     long long cnt[2];
     read_counts(e, cnt);
@@ -1165,10 +1225,11 @@ int hddm_fgmres(hddm_engine* e, const double* b, double* x, double tol, int max_
           // Z_j = M(V_j): K DDM sweeps (precondition, ddm.cpp:280-287)
           e->reset_state();
           CK(cudaMemsetAsync(e->d_counts, 0, 2 * sizeof(long long), st));
-          StepArgs A0 = e->step_args(1, e->V[j]);
+          CK(cudaMemcpyAsync(e->d_f, e->V[j], n * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+          StepArgs A0 = e->step_args(1, e->d_f);
           launch_fany(A0, st);
           const double ts = now_ms();
-          for (int s = 1; s <= ksteps; ++s) e->enqueue_step(s, e->V[j]);
+          for (int s = 1; s <= ksteps; ++s) e->run_step(s);
           CK(cudaMemcpyAsync(e->Z[j], e->d_asm, n * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
           // w = A Z_j
           cplx* w = e->V[j + 1];
@@ -1284,34 +1345,12 @@ int hddm_class_solve(hddm_engine* e, int c, const double* b, double* x, double* 
     CK(cudaMemcpyAsync(e->d_Z[0], zc.data(), sizeof(int) * e->nsub, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(e->d_act_ptr, aptr.data(), sizeof(int) * (e->ncls + 1), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(e->d_act_list, alist.data(), sizeof(int), cudaMemcpyHostToDevice, st));
-    launch_solve(e->solve_args(e->d_B, e->d_U[0], e->d_Y), e->plan, e->ncls, 1, 1, st);
-    CheckArgs C;
-    C.nw = e->nw;
-    C.wnx = e->wnx;
-    C.wny = e->wny;
-    C.gnx = e->S.gnx;
-    C.nring = e->Y.nring;
-    C.ih2 = 1.0 / (e->S.h * e->S.h);
-    C.sub = e->d_sub;
-    C.sa = e->d_sa;
-    C.sa_stride = e->sa_stride;
-    C.k2 = e->d_k2;
-    C.perm = e->d_perm;
-    C.pinv = e->d_pinv;
-    C.zc = e->d_Z[0];
-    C.nsub = e->nsub;
-    C.B = e->d_B;
-    C.X = e->d_U[0];
-    C.part = e->d_part_chk;
-    C.nchunk = e->nchunk;
-    C.rel = e->d_rel;
-    C.refine_flag = e->d_refine;
-    C.max_rel = e->d_maxrel;
-    launch_check(C, st);
+    launch_solve(e->solve_args(e->d_B, e->d_U[0], e->d_Y), e->plan, e->ncls, 1, st);
+    e->host_refine(e->d_B, e->d_U[0], e->d_Z[0]);
     std::vector<cplx> xf(e->nw);
     double rel = 0;
     CK(cudaMemcpyAsync(xf.data(), e->d_U[0] + size_t(t) * e->nw, e->nw * sizeof(cplx), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&rel, e->d_rel + t, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&rel, e->d_relcur + t, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     for (int k = 0; k < e->nw; ++k) {
       const int node = e->Y.perm[k];
@@ -1347,6 +1386,47 @@ int hddm_stage_times(hddm_engine* e, double* ms, long long* count, int cap, int*
 }
 
 long long hddm_launch_count(const hddm_engine* e) { return e->launches; }
+
+int hddm_time_solve(hddm_engine* e, int reps, double* ms_per_solve) {
+  return guarded(e, [&] {
+    // steady state: every subdomain active, right-hand sides of the last step
+    std::vector<int> aptr(e->ncls + 1), alist(e->nsub);
+    for (int c = 0; c <= e->ncls; ++c) aptr[c] = e->S.cls_ptr[c];
+    for (int k = 0; k < e->nsub; ++k) alist[k] = e->S.cls_members[k];
+    cudaStream_t st = e->st;
+    CK(cudaMemcpyAsync(e->d_act_ptr, aptr.data(), sizeof(int) * (e->ncls + 1), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(e->d_act_list, alist.data(), sizeof(int) * e->nsub, cudaMemcpyHostToDevice, st));
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    launch_solve(e->solve_args(e->d_B, e->d_C, e->d_Y), e->plan, e->ncls, e->nsub, st);
+    CK(cudaStreamEndCapture(st, &g));
+    cudaGraphExec_t x;
+    CK(cudaGraphInstantiate(&x, g, 0));
+    CK(cudaGraphDestroy(g));
+    CK(cudaGraphLaunch(x, st));  // warm-up
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a, st));
+    for (int r = 0; r < reps; ++r) CK(cudaGraphLaunch(x, st));
+    CK(cudaEventRecord(b, st));
+    CK(cudaEventSynchronize(b));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    *ms_per_solve = ms / std::max(reps, 1);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaGraphExecDestroy(x);
+  });
+}
+
+int hddm_solve_launches(const hddm_engine* e) { return solve_launch_count(e->plan); }
+
+int hddm_refine_stats(const hddm_engine* e, double* max_local_relres, int* corrections) {
+  *max_local_relres = e->last_max_rel;
+  *corrections = e->last_refine_count;
+  return HDDM_OK;
+}
 
 const char* hddm_stage_name(int i) { return i >= 0 && i < kStages ? kStageNames[i] : ""; }
 

@@ -29,47 +29,26 @@ struct SolveArgs {
   int nw, nring;
 };
 
+// One level of the level-synchronous sweeps: a flat list of output items
+// (supernode, row/column index) or (leaf, 0) that are independent given the
+// previous levels. Threads are laid out class-major, then item, then member.
 struct SolveLevel {
-  int ntask = 0;
-  Task* d_tasks = nullptr;
-  int ntask32 = 0;          // backward pull: 32-column tasks
-  Task* d_tasks32 = nullptr;
-};
-
-// a maximal ND subtree solved by one CTA: positions [p0, p0+np), phases
-// [ph0, ph0+nph) bottom-up
-struct SubtreeInfo {
-  int p0, np, ph0, nph;
-};
-struct Phase {
-  int kind, it0, nit, pad;  // kind 0 leaves (items (leaf, 0)), 1 separators (items (sn, i))
-  int ic0, nic, pad1, pad2; // kind 0: leaf columns (items (leaf, j)) for the backward blocks
-};
-struct SubtreeArgs {
-  const SubtreeInfo* st;
-  const Phase* ph;
-  const int2* items;
-  int np_max, items_max, seg_max;
-  int dbg;  // profiling only (HDDM_DEBUG_SKIP): bit0/1 skip fwd leaf/sep phases, bit2/3 bwd
-};
-// classes grouped by member count; MC = members per shared-memory pass
-struct SolveBucket {
-  int mc = 1, ncls = 0;
-  int* d_cls = nullptr;
+  int nitem = 0;
+  int2* d_items = nullptr;
+  bool warp_rows = false;  // forward: long incoming runs -> warp per row
 };
 
 struct SolvePlan {
-  int* d_wprefix = nullptr;  // per class: first warp of the (class, subtree, rhs) list
-  int nsubtree = 0;
-  SubtreeArgs sub{};
-  std::vector<SolveBucket> buckets;
-  std::vector<SolveLevel> fwd, bwd;  // separators above the subtrees
-  int seg_max_top = 0;               // most segments of any top-level row
+  SolveLevel fwd_leaf;                 // leaves: band forward substitution
+  std::vector<SolveLevel> fwd;         // separator rows by height (pull, then diag)
+  std::vector<SolveLevel> bwd;         // separator columns by depth (pull, then diag)
+  SolveLevel bwd_leafcol;              // leaf columns: w = Dinv z - B^T x
+  SolveLevel bwd_leaf;                 // leaves: band back-substitution
 };
 
 // max_rhs bounds the number of active right-hand sides over all classes
-void launch_solve(const SolveArgs& A, const SolvePlan& P, int ncls, int max_members,
-                  int max_rhs, cudaStream_t st);
+void launch_solve(const SolveArgs& A, const SolvePlan& P, int ncls, int max_rhs,
+                  cudaStream_t st);
 int solve_launch_count(const SolvePlan& P);
 
 // ------------------------------------------------------------------ factor
@@ -148,6 +127,7 @@ struct CheckArgs {
   const int* perm;
   const int* pinv;
   const int* zc;      // per RHS: 1 = inactive
+  const int* only;    // if set: process RHS t only when only[t] != 0 (refinement re-checks)
   int nsub;
   const cplx* B;
   const cplx* X;
@@ -157,7 +137,44 @@ struct CheckArgs {
   int* refine_flag;  // set when any rel > 1e-11
   double* max_rel;
 };
-void launch_check(const CheckArgs& A, cudaStream_t st);
+void launch_check(const CheckArgs& A, cudaStream_t st);           // partials + per-RHS rel
+void launch_check_partials(const CheckArgs& A, cudaStream_t st);  // partials only
+
+// Iterative refinement on device (refine, proj/src/sparse.cpp:268-292): per RHS
+// state after the first solve; corrections run inside a conditional WHILE graph
+// node while any RHS still needs one.
+struct RefineArgs {
+  int nsub, ncls, nw, wnx, wny, gnx, nchunk;
+  double ih2;
+  const DevSub* sub;
+  const cplx* sa;
+  int sa_stride;
+  const double* k2;
+  const int* perm;
+  const int* pinv;
+  const int* zc;
+  const cplx* B;
+  cplx* X;
+  cplx* R;            // residual vectors (correction right-hand sides)
+  cplx* C;            // corrections
+  const double* part; // check partials
+  double* rel_cur;    // per RHS: last accepted relative residual
+  int* need;          // per RHS: still refining
+  int* ncorr;         // per RHS: corrections applied
+  int* undo;          // per RHS: last correction to be undone
+  int* any;           // device flag: some RHS needs a correction
+  long long* nfix;    // total corrections applied (diagnostics)
+  const int* cls_ptr;
+  const int* cls_mem;
+  int* act_ptr;
+  int* act_list;
+  unsigned long long cond;  // cudaGraphConditionalHandle (0: not in a graph)
+};
+void launch_refine_init(const RefineArgs& R, cudaStream_t st);   // after the first check
+void launch_refine_prep(const RefineArgs& R, cudaStream_t st);   // act lists + residuals
+void launch_refine_apply(const RefineArgs& R, cudaStream_t st);  // X += C
+void launch_refine_decide(const RefineArgs& R, cudaStream_t st); // after the re-check
+void launch_refine_undo(const RefineArgs& R, cudaStream_t st);
 
 // ------------------------------------------------------------------ global
 struct GlobalArgs {

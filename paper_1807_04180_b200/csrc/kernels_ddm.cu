@@ -271,10 +271,37 @@ void launch_accumulate(const StepArgs& A, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------ residual check
+// (A x)_pos for the J-scaled assembled matrix of subdomain t's window
+// (discretize.cpp:98-160): identity ring rows, ring columns dropped.
+__device__ __forceinline__ cplx ax_row(const cplx* __restrict__ X, int pos, int wnx, int wny,
+                                       int gnx, double ih2, const DevSub& T, const cplx* sa,
+                                       const double* k2g, const int* perm, const int* pinv) {
+  const int node = perm[pos];
+  const int lp = node % wnx, lq = node / wnx;
+  if (lp == 0 || lq == 0 || lp == wnx - 1 || lq == wny - 1) return X[pos];
+  const cplx* a1n = sa;
+  const cplx* ia1h = sa + wnx;
+  const cplx* a2n = sa + 2 * wnx;
+  const cplx* ia2h = sa + 2 * wnx + wny;
+  const cplx ew = cscale(cmul(a2n[lq], ia1h[lp - 1]), ih2);
+  const cplx ee = cscale(cmul(a2n[lq], ia1h[lp]), ih2);
+  const cplx es = cscale(cmul(a1n[lp], ia2h[lq - 1]), ih2);
+  const cplx en = cscale(cmul(a1n[lp], ia2h[lq]), ih2);
+  const double k2 = k2g[(long long)(T.wy0 + lq) * gnx + T.wx0 + lp];
+  const cplx diag = cadd(cmk(-(ew.x + ee.x + es.x + en.x), -(ew.y + ee.y + es.y + en.y)),
+                         cscale(cmul(a1n[lp], a2n[lq]), k2));
+  cplx ax = cmul(diag, X[pos]);
+  if (lq > 1) cfma(ax, es, X[pinv[node - wnx]]);
+  if (lp > 1) cfma(ax, ew, X[pinv[node - 1]]);
+  if (lp < wnx - 2) cfma(ax, ee, X[pinv[node + 1]]);
+  if (lq < wny - 2) cfma(ax, en, X[pinv[node + wnx]]);
+  return ax;
+}
+
 __global__ void __launch_bounds__(256) k_check(CheckArgs A) {
   __shared__ double sh[32];
   const int t = blockIdx.y;
-  const bool act = !A.zc[t];
+  const bool act = A.only ? A.only[t] != 0 : !A.zc[t];
   double r2 = 0, b2 = 0;
   if (act) {
     const cplx* X = A.X + (long long)t * A.nw;
@@ -290,26 +317,7 @@ __global__ void __launch_bounds__(256) k_check(CheckArgs A) {
     for (int pos = p0 + threadIdx.x; pos < p1; pos += blockDim.x) {
       const cplx b = Bv[pos];
       b2 += cnorm2(b);
-      const int node = A.perm[pos];
-      const int lp = node % A.wnx, lq = node / A.wnx;
-      cplx ax;
-      if (lp == 0 || lq == 0 || lp == A.wnx - 1 || lq == A.wny - 1) {
-        ax = X[pos];
-      } else {
-        // J-scaled row of the assembled matrix (discretize.cpp:131-158)
-        const cplx ew = cscale(cmul(a2n[lq], ia1h[lp - 1]), A.ih2);
-        const cplx ee = cscale(cmul(a2n[lq], ia1h[lp]), A.ih2);
-        const cplx es = cscale(cmul(a1n[lp], ia2h[lq - 1]), A.ih2);
-        const cplx en = cscale(cmul(a1n[lp], ia2h[lq]), A.ih2);
-        const double k2 = A.k2[(long long)(T.wy0 + lq) * A.gnx + T.wx0 + lp];
-        const cplx diag = cadd(cmk(-(ew.x + ee.x + es.x + en.x), -(ew.y + ee.y + es.y + en.y)),
-                               cscale(cmul(a1n[lp], a2n[lq]), k2));
-        ax = cmul(diag, X[pos]);
-        if (lq > 1) cfma(ax, es, X[A.pinv[node - A.wnx]]);
-        if (lp > 1) cfma(ax, ew, X[A.pinv[node - 1]]);
-        if (lp < A.wnx - 2) cfma(ax, ee, X[A.pinv[node + 1]]);
-        if (lq < A.wny - 2) cfma(ax, en, X[A.pinv[node + A.wnx]]);
-      }
+      const cplx ax = ax_row(X, pos, A.wnx, A.wny, A.gnx, A.ih2, T, sa, A.k2, A.perm, A.pinv);
       r2 += cnorm2(csub(b, ax));
     }
   }
@@ -330,7 +338,7 @@ __global__ void k_check_finish(CheckArgs A, int nsub) {
     }
     const double rel = b2 > 0 ? sqrt(r2) / sqrt(b2) : 0.0;
     A.rel[t] = rel;
-    if (rel > 1e-11) atomicOr(A.refine_flag, 1);
+    if (rel > 1e-11) atomicAdd(A.refine_flag, 1);
     // max_rel: deterministic (max is order-free); atomicMax on the bit pattern of a
     // nonnegative double preserves ordering
     atomicMax(reinterpret_cast<unsigned long long*>(A.max_rel),
@@ -338,10 +346,161 @@ __global__ void k_check_finish(CheckArgs A, int nsub) {
   }
 }
 
+void launch_check_partials(const CheckArgs& A, cudaStream_t st) {
+  dim3 g(A.nchunk, A.nsub);
+  k_check<<<g, 256, 0, st>>>(A);
+}
+
 void launch_check(const CheckArgs& A, cudaStream_t st) {
   dim3 g(A.nchunk, A.nsub);
   k_check<<<g, 256, 0, st>>>(A);
   k_check_finish<<<1, 256, 0, st>>>(A, A.nsub);
+}
+
+// ------------------------------------------------------------ refinement
+__device__ __forceinline__ void set_cond(unsigned long long h, int v) {
+  if (h) cudaGraphSetConditional(cudaGraphConditionalHandle(h), unsigned(v));
+}
+
+// first pass done: rel[t] from the check partials; start refining RHS above 1e-11
+__global__ void k_refine_init(RefineArgs R) {
+  __shared__ int any;
+  if (threadIdx.x == 0) any = 0;
+  __syncthreads();
+  for (int t = threadIdx.x; t < R.nsub; t += blockDim.x) {
+    double r2 = 0, b2 = 0;
+    for (int k = 0; k < R.nchunk; ++k) {
+      r2 += R.part[((long long)t * R.nchunk + k) * 2];
+      b2 += R.part[((long long)t * R.nchunk + k) * 2 + 1];
+    }
+    const double rel = b2 > 0 ? sqrt(r2) / sqrt(b2) : 0.0;
+    const int nd = (!R.zc[t] && b2 > 0 && rel > 1e-11) ? 1 : 0;
+    R.rel_cur[t] = rel;
+    R.need[t] = nd;
+    R.ncorr[t] = 0;
+    R.undo[t] = 0;
+    if (nd) atomicOr(&any, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *R.any = any;
+    set_cond(R.cond, any);
+  }
+}
+
+// act lists of the RHS still refining, in class order
+__global__ void k_refine_lists(RefineArgs R) {
+  extern __shared__ int sh[];
+  for (int c = threadIdx.x; c < R.ncls; c += blockDim.x) {
+    int cnt = 0;
+    for (int k = R.cls_ptr[c]; k < R.cls_ptr[c + 1]; ++k) cnt += R.need[R.cls_mem[k]];
+    sh[c] = cnt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int c = 0; c < R.ncls; ++c) {
+      R.act_ptr[c] = acc;
+      acc += sh[c];
+    }
+    R.act_ptr[R.ncls] = acc;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < R.ncls; c += blockDim.x) {
+    int o = R.act_ptr[c];
+    for (int k = R.cls_ptr[c]; k < R.cls_ptr[c + 1]; ++k)
+      if (R.need[R.cls_mem[k]]) R.act_list[o++] = R.cls_mem[k];
+  }
+}
+
+// R = B - A X for the refining RHS
+__global__ void __launch_bounds__(256) k_refine_resid(RefineArgs R) {
+  const int t = blockIdx.y;
+  if (!R.need[t]) return;
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= R.nw) return;
+  const DevSub T = R.sub[t];
+  const cplx* X = R.X + (long long)t * R.nw;
+  const cplx ax = ax_row(X, pos, R.wnx, R.wny, R.gnx, R.ih2, T, R.sa + (long long)t * R.sa_stride,
+                         R.k2, R.perm, R.pinv);
+  R.R[(long long)t * R.nw + pos] = csub(R.B[(long long)t * R.nw + pos], ax);
+}
+
+// X += C for the refining RHS
+__global__ void __launch_bounds__(256) k_refine_apply(RefineArgs R) {
+  const int t = blockIdx.y;
+  if (!R.need[t]) return;
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= R.nw) return;
+  const long long p = (long long)t * R.nw + pos;
+  R.X[p] = cadd(R.X[p], R.C[p]);
+}
+
+// after the re-check: the reference's stagnation / stopping rules
+__global__ void k_refine_decide(RefineArgs R) {
+  __shared__ int any;
+  if (threadIdx.x == 0) any = 0;
+  __syncthreads();
+  for (int t = threadIdx.x; t < R.nsub; t += blockDim.x) {
+    if (!R.need[t]) continue;
+    const int nc = ++R.ncorr[t];
+    atomicAdd(reinterpret_cast<unsigned long long*>(R.nfix), 1ULL);
+    if (nc >= 12) {  // the reference's loop ends after its 12th correction
+      R.need[t] = 0;
+      continue;
+    }
+    double r2 = 0, b2 = 0;
+    for (int k = 0; k < R.nchunk; ++k) {
+      r2 += R.part[((long long)t * R.nchunk + k) * 2];
+      b2 += R.part[((long long)t * R.nchunk + k) * 2 + 1];
+    }
+    const double rn = b2 > 0 ? sqrt(r2) / sqrt(b2) : 0.0;
+    const double rel = R.rel_cur[t];
+    if (rn >= 0.5 * rel) {  // stagnation: stop, undoing a correction that hurt
+      if (rn > rel) R.undo[t] = 1;
+      R.rel_cur[t] = rn < rel ? rn : rel;  // refine returns min(r, rel)
+      R.need[t] = 0;
+    } else {
+      R.rel_cur[t] = rn;
+      if (rn <= 1e-11) R.need[t] = 0;
+    }
+    if (R.need[t]) atomicOr(&any, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *R.any = any;
+    set_cond(R.cond, any);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_refine_undo(RefineArgs R) {
+  const int t = blockIdx.y;
+  if (!R.undo[t]) return;
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= R.nw) return;
+  const long long p = (long long)t * R.nw + pos;
+  R.X[p] = csub(R.X[p], R.C[p]);
+  if (pos == 0) {}  // flag cleared by the next init
+}
+
+void launch_refine_init(const RefineArgs& R, cudaStream_t st) {
+  k_refine_init<<<1, 256, 0, st>>>(R);
+}
+void launch_refine_prep(const RefineArgs& R, cudaStream_t st) {
+  k_refine_lists<<<1, 256, sizeof(int) * R.ncls, st>>>(R);
+  dim3 g((R.nw + 255) / 256, R.nsub);
+  k_refine_resid<<<g, 256, 0, st>>>(R);
+}
+void launch_refine_apply(const RefineArgs& R, cudaStream_t st) {
+  dim3 g((R.nw + 255) / 256, R.nsub);
+  k_refine_apply<<<g, 256, 0, st>>>(R);
+}
+void launch_refine_decide(const RefineArgs& R, cudaStream_t st) {
+  k_refine_decide<<<1, 256, 0, st>>>(R);
+}
+void launch_refine_undo(const RefineArgs& R, cudaStream_t st) {
+  dim3 g((R.nw + 255) / 256, R.nsub);
+  k_refine_undo<<<g, 256, 0, st>>>(R);
 }
 
 // ------------------------------------------------------------ global stencil

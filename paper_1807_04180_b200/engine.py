@@ -144,6 +144,9 @@ def load_library(path: str = LIB_PATH):
         "hddm_set_timing": (C.c_int, [vp, C.c_int]),
         "hddm_stage_times": (C.c_int, [vp, dp, P(C.c_longlong), C.c_int, ip]),
         "hddm_launch_count": (C.c_longlong, [vp]),
+        "hddm_refine_stats": (C.c_int, [vp, dp, ip]),
+        "hddm_time_solve": (C.c_int, [vp, C.c_int, dp]),
+        "hddm_solve_launches": (C.c_int, [vp]),
         "hddm_stage_name": (C.c_char_p, [C.c_int]),
         "hddm_stream": (vp, [vp]),
     }
@@ -403,6 +406,21 @@ class DdmEngine:
                                               C.byref(n)))
         return {self.lib.hddm_stage_name(i).decode(): (float(buf[i]), int(cnt[i]))
                 for i in range(n.value)}
+
+    def refine_stats(self):
+        """(max local-solve relres, number of solves above 1e-11) of the last call."""
+        m, n = C.c_double(), C.c_int()
+        self._check(self.lib.hddm_refine_stats(self.h, C.byref(m), C.byref(n)))
+        return m.value, n.value
+
+    def time_solve(self, reps: int = 10) -> float:
+        """Average device ms of one batched solve stage (steady state)."""
+        ms = C.c_double()
+        self._check(self.lib.hddm_time_solve(self.h, reps, C.byref(ms)))
+        return ms.value
+
+    def solve_launches(self) -> int:
+        return int(self.lib.hddm_solve_launches(self.h))
 
     def launch_count(self) -> int:
         return int(self.lib.hddm_launch_count(self.h))
