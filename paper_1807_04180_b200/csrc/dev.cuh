@@ -47,6 +47,15 @@ __device__ __forceinline__ cplx ldg(const cplx* p) { return __ldg(p); }
 // per-subdomain vectors (reused across levels) stay cached
 __device__ __forceinline__ cplx ldf(const cplx* p) { return __ldcs(p); }
 
+// Non-blocking prefetch of the 128-byte lines covering [p, p + n) into L1.
+__device__ __forceinline__ void prefetch_lines(const cplx* p, int n) {
+  const char* a = reinterpret_cast<const char*>(p);
+  const char* e = reinterpret_cast<const char*>(p + n);
+  for (const char* q = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(a) & ~uintptr_t(127));
+       q < e; q += 128)
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
+}
+
 // Asynchronous bulk prefetch of a contiguous global range into L2 (TMA path,
 // sm_90+). p must be 16-byte aligned and bytes a multiple of 16.
 __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {

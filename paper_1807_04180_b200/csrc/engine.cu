@@ -126,6 +126,10 @@ struct hddm_engine {
   // one CUDA graph per step variant (step 1; s >= 2 by s mod 3), each with a
   // conditional WHILE node running the refinement corrections on demand
   cudaStream_t st2 = nullptr;
+  std::vector<cudaStream_t> cls_st;     // per-class streams for the step graphs
+  std::vector<cudaEvent_t> cls_ev;
+  cudaEvent_t fork_ev = nullptr;
+  bool per_class_streams = true;
   cudaGraphExec_t step_exec[4] = {};
   int step_kernels = 0;
   // global
@@ -183,6 +187,9 @@ struct hddm_engine {
     if (h_scal) cudaFreeHost(h_scal);
     for (auto& g : step_exec)
       if (g) cudaGraphExecDestroy(g);
+    for (auto& x : cls_st) cudaStreamDestroy(x);
+    for (auto& x : cls_ev) cudaEventDestroy(x);
+    if (fork_ev) cudaEventDestroy(fork_ev);
     if (st2) cudaStreamDestroy(st2);
     if (st) cudaStreamDestroy(st);
   }
@@ -264,6 +271,7 @@ void hddm_engine::create(const hddm_problem& p) {
   CK(cudaSetDevice(dev));
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+  per_class_streams = std::getenv("HDDM_SINGLE_STREAM") == nullptr;
   CK(cudaMallocHost(&h_scal, 64 * sizeof(double)));
   nsub = S.n1 * S.n2;
   ncls = S.ncls;
@@ -531,14 +539,56 @@ void hddm_engine::build_plan() {
     long tot = 0;
     for (const int2& it : v) tot += Y.run_off[Y.sn[it.x].c0 + it.y + 1] - Y.run_off[Y.sn[it.x].c0 + it.y];
     L.warp_rows = tot > 128L * long(v.size());  // average run longer than 4 warp strides
+    const long avg = tot / long(v.size());
+    L.group = avg > 128 ? 32 : 1;  // sub-warp groups measured slower than thread-per-row
+    if (const char* g = std::getenv("HDDM_FWD_GROUP")) L.group = std::atoi(g);
+    {
+      int nmax = 0;
+      std::vector<int2> seps;
+      for (const int2& it : v)
+        if (it.y == 0) seps.push_back(make_int2(it.x, 0));
+      for (const int2& sp : seps) nmax = std::max(nmax, Y.sn[sp.x].n);
+      if (nmax <= 32 && std::getenv("HDDM_SMALL")) {  // measured slower: opt-in
+        L.small_g = nmax <= 8 ? 8 : nmax <= 16 ? 16 : 32;
+        L.nsmall = int(seps.size());
+        L.d_small = upload(seps);
+      }
+    }
+    long dsum = 0;
+    for (const int2& it : v) dsum += it.y;
+    L.warp_diag = dsum > 48L * long(v.size());   // average inverse row longer than 48
     plan.fwd.push_back(L);
   }
   for (int d = 0; d <= Y.max_depth; ++d) {
-    std::vector<int2> v;
+    std::vector<int2> v, ch;
+    long rows = 0, cols = 0, nmax = 0;
     for (int s = 0; s < nsn; ++s)
-      if (Y.sn[s].kind == 1 && Y.sn[s].depth == d)
+      if (Y.sn[s].kind == 1 && Y.sn[s].depth == d) {
         for (int i = 0; i < Y.sn[s].n; ++i) v.push_back(make_int2(s, i));
-    if (!v.empty()) plan.bwd.push_back(level(v));
+        for (int i = 0; i < Y.sn[s].n; i += 32) ch.push_back(make_int2(s, i));
+        long nr = 0;
+        for (int b = Y.sn[s].blk0; b < Y.sn[s].blk0 + Y.sn[s].nblk; ++b) nr += Y.blk[b].nr;
+        rows += nr * Y.sn[s].n;
+        cols += Y.sn[s].n;
+        nmax = std::max<long>(nmax, Y.sn[s].n);
+      }
+    if (v.empty()) continue;
+    SolveLevel L = level(v);
+    if (nmax <= 32 && std::getenv("HDDM_SMALL")) {  // measured slower: opt-in
+      std::vector<int2> seps;
+      for (const int2& it : v)
+        if (it.y == 0) seps.push_back(make_int2(it.x, 0));
+      L.small_g = nmax <= 8 ? 8 : nmax <= 16 ? 16 : 32;
+      L.nsmall = int(seps.size());
+      L.d_small = upload(seps);
+    }
+    L.warp_rows = rows > 64L * cols;  // more than 64 rows per column
+    L.warp_diag = nmax > 48;
+    if (L.warp_rows || L.warp_diag) {
+      L.nchunk = int(ch.size());
+      L.d_chunks = upload(ch);
+    }
+    plan.bwd.push_back(L);
   }
 }
 
@@ -833,7 +883,29 @@ void hddm_engine::enqueue_step_front(int s, cudaStream_t stream, unsigned long l
   const StepArgs A = step_args(s, d_f);
   launch_flags(A, ncls, stream);
   launch_gather(A, stream);
-  launch_solve(solve_args(d_B, A.Ucur, d_Y), plan, ncls, nsub, stream);
+  if (per_class_streams && stream == st && ncls > 1) {
+    // fork: every class runs its level chain on its own stream, so its
+    // vectors stay L2-resident between consecutive levels; join afterwards
+    if (cls_st.empty()) {
+      cls_st.resize(ncls);
+      cls_ev.resize(ncls);
+      for (int c = 0; c < ncls; ++c) {
+        CK(cudaStreamCreateWithFlags(&cls_st[c], cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&cls_ev[c], cudaEventDisableTiming));
+      }
+      CK(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(fork_ev, stream));
+    const SolveArgs SA = solve_args(d_B, A.Ucur, d_Y);
+    for (int c = 0; c < ncls; ++c) {
+      CK(cudaStreamWaitEvent(cls_st[c], fork_ev, 0));
+      launch_solve_class(SA, plan, c, S.cls_ptr[c + 1] - S.cls_ptr[c], cls_st[c]);
+      CK(cudaEventRecord(cls_ev[c], cls_st[c]));
+    }
+    for (int c = 0; c < ncls; ++c) CK(cudaStreamWaitEvent(stream, cls_ev[c], 0));
+  } else {
+    launch_solve(solve_args(d_B, A.Ucur, d_Y), plan, ncls, nsub, stream);
+  }
   launch_check(check_args(d_B, A.Ucur, A.zc, nullptr), stream);
   launch_refine_init(refine_args(d_B, A.Ucur, A.zc, cond), stream);
 }
@@ -889,6 +961,25 @@ void hddm_engine::build_step_graph(int v) {
 }
 
 void hddm_engine::run_step(int s) {
+  if (!step_exec[0] && !std::getenv("HDDM_NO_GRAPHS"))
+    for (int v = 0; v < 4; ++v) build_step_graph(v);  // all variants up front
+  static const bool no_graphs = std::getenv("HDDM_NO_GRAPHS") != nullptr;
+  if (no_graphs) {
+    // direct launches (profiling aid): same kernels, refinement driven from the host
+    enqueue_step_front(s, st, 0);
+    const StepArgs A = step_args(s, d_f);
+    for (int it = 0; it < 13; ++it) {
+      int any = 0;
+      CK(cudaMemcpyAsync(&any, d_any, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (!any) break;
+      enqueue_refine_body(s, st, 0);
+    }
+    launch_accumulate(A, st);
+    launches += 1 + 2 + solve_launches() + 2 + 1 + 1;
+    last_step = s;
+    return;
+  }
   const int v = variant_of(s);
   if (!step_exec[v]) build_step_graph(v);
   CK(cudaGraphLaunch(step_exec[v], st));

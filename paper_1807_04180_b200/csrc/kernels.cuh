@@ -35,7 +35,14 @@ struct SolveArgs {
 struct SolveLevel {
   int nitem = 0;
   int2* d_items = nullptr;
-  bool warp_rows = false;  // forward: long incoming runs -> warp per row
+  bool warp_rows = false;  // long pulls: forward warp per row / backward split rows
+  int group = 1;           // forward pull: lanes per row (1, 4, 8, 16, 32)
+  bool warp_diag = false;  // large separators: split the dense-inverse products
+  int small_g = 0;         // >0: fused pull+diagonal, this many lanes per separator
+  int nsmall = 0;          // (separator, 0) items of the fused kernels
+  int2* d_small = nullptr;
+  int nchunk = 0;          // backward split variants: (supernode, 32-column chunk) items
+  int2* d_chunks = nullptr;
 };
 
 struct SolvePlan {
@@ -50,6 +57,8 @@ struct SolvePlan {
 void launch_solve(const SolveArgs& A, const SolvePlan& P, int ncls, int max_rhs,
                   cudaStream_t st);
 int solve_launch_count(const SolvePlan& P);
+void launch_solve_class(const SolveArgs& A, const SolvePlan& P, int c, int members,
+                        cudaStream_t st);
 
 // ------------------------------------------------------------------ factor
 struct FactorArgs {
