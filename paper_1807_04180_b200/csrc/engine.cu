@@ -536,6 +536,15 @@ void hddm_engine::build_plan() {
         for (int i = 0; i < Y.sn[s].n; ++i) v.push_back(make_int2(s, i));
     if (v.empty()) continue;
     SolveLevel L = level(v);
+    {
+      std::vector<int4> rec(v.size());
+      for (size_t k = 0; k < v.size(); ++k) {
+        const int pos = Y.sn[v[k].x].c0 + v[k].y;
+        const long long ro = Y.run_off[pos];
+        rec[k] = make_int4(pos, int(Y.run_off[pos + 1] - ro), int(ro & 0xffffffffLL), int(ro >> 32));
+      }
+      L.d_rec = upload(rec);
+    }
     long tot = 0;
     for (const int2& it : v) tot += Y.run_off[Y.sn[it.x].c0 + it.y + 1] - Y.run_off[Y.sn[it.x].c0 + it.y];
     L.warp_rows = tot > 128L * long(v.size());  // average run longer than 4 warp strides
@@ -702,6 +711,10 @@ SolveArgs hddm_engine::solve_args(const cplx* Bp, cplx* X, cplx* Yp) {
   A.Y = Yp;
   A.nw = nw;
   A.nring = Y.nring;
+  static const int mm = std::getenv("HDDM_MEMBER_MAJOR") ? std::atoi(std::getenv("HDDM_MEMBER_MAJOR")) : 0;
+  A.member_major = mm;
+  static const int bmm = std::getenv("HDDM_BWD_MM") ? std::atoi(std::getenv("HDDM_BWD_MM")) : 0;
+  A.bwd_mm = bmm;
   return A;
 }
 

@@ -27,6 +27,8 @@ struct SolveArgs {
   cplx* X;             // solutions (factor order), stride nw
   cplx* Y;             // scratch, stride nw
   int nw, nring;
+  int member_major;  // thread order: 0 class/item/member, 1 class/member/item
+  int bwd_mm;        // backward kernels member-major
 };
 
 // One level of the level-synchronous sweeps: a flat list of output items
@@ -35,6 +37,7 @@ struct SolveArgs {
 struct SolveLevel {
   int nitem = 0;
   int2* d_items = nullptr;
+  int4* d_rec = nullptr;   // forward: (position, run length, run offset lo, hi) per item
   bool warp_rows = false;  // long pulls: forward warp per row / backward split rows
   int group = 1;           // forward pull: lanes per row (1, 4, 8, 16, 32)
   bool warp_diag = false;  // large separators: split the dense-inverse products

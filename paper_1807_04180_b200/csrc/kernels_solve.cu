@@ -44,8 +44,35 @@ __device__ __forceinline__ bool decode(const SolveArgs& A, int ncls, long long i
   c = lo;
   const int m = ap[c + 1] - ap[c];
   const long long r = idx - (long long)(ap[c] - a0) * nitem;
-  item = int(r / m);
-  t = A.act_list[ap[c] + int(r - (long long)item * m)];
+  if (A.member_major) {  // consecutive threads: consecutive items of one RHS
+    const int k = int(r / nitem);
+    item = int(r - (long long)k * nitem);
+    t = A.act_list[ap[c] + k];
+  } else {               // consecutive threads: the members of one item
+    item = int(r / m);
+    t = A.act_list[ap[c] + int(r - (long long)item * m)];
+  }
+  return true;
+}
+
+// member-major decode: consecutive threads walk consecutive items of ONE right-
+// hand side (backward sweeps: a warp covers consecutive columns, so the
+// ancestor value x_r is a broadcast and the factor row a coalesced read)
+__device__ __forceinline__ bool decode_mm(const SolveArgs& A, int ncls, long long idx, int nitem,
+                                          int& c, int& item, int& t) {
+  const int* ap = A.act_ptr;
+  const int a0 = ap[0];
+  if (idx >= (long long)(ap[ncls] - a0) * nitem) return false;
+  int lo = 0, hi = ncls - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if ((long long)(ap[mid] - a0) * nitem <= idx) lo = mid; else hi = mid - 1;
+  }
+  c = lo;
+  const long long r = idx - (long long)(ap[c] - a0) * nitem;
+  const int k = int(r / nitem);
+  item = int(r - (long long)k * nitem);
+  t = A.act_list[ap[c] + k];
   return true;
 }
 
@@ -170,39 +197,35 @@ __global__ void __launch_bounds__(kThreads) k_fwd_leaf(SolveArgs A, int ncls, co
   }
 }
 
-// separator rows, forward pull: Y[r] = B[r] - run(r) . X[src] (thread per row)
-__global__ void __launch_bounds__(kThreads) k_fwd_pull(SolveArgs A, int ncls, const int2* items,
+// separator rows, forward pull: Y[r] = B[r] - run(r) . X[src] (thread per row).
+// rec[item] = (position, run length, run offset lo, hi): one load of setup.
+__global__ void __launch_bounds__(kThreads) k_fwd_pull(SolveArgs A, int ncls, const int4* rec,
                                                        int nitem) {
   int c, it, t;
   if (!decode(A, ncls, (long long)blockIdx.x * blockDim.x + threadIdx.x, nitem, c, it, t)) return;
-  const int2 item = items[it];
-  const int pos = A.sn[item.x].c0 + item.y;
-  const long long r0 = A.run_off[pos];
-  const int total = int(A.run_off[pos + 1] - r0);
+  const int4 R = __ldg(rec + it);
+  const long long r0 = (long long)(unsigned)R.z | ((long long)R.w << 32);
   const cplx* run = A.vals + (long long)c * A.nvals + r0;
   const long long base = (long long)t * A.nw;
-  const cplx s = gather_dot<4>(run, A.zidx + r0, 0, total, 1, A.X + base);
-  A.Y[base + pos] = csub(A.B[base + pos], s);
+  const cplx s = gather_dot<4>(run, A.zidx + r0, 0, R.y, 1, A.X + base);
+  A.Y[base + R.x] = csub(A.B[base + R.x], s);
 }
 
 // separator rows with long runs (top levels): one WARP per (class, row,
 // member); lanes stride the run (coalesced), zidx gives each element's source.
 __global__ void __launch_bounds__(kThreads) k_fwd_pull_warp(SolveArgs A, int ncls,
-                                                            const int2* items, int nitem) {
+                                                            const int4* rec, int nitem) {
   int c, it, t;
   const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (!decode(A, ncls, w, nitem, c, it, t)) return;
-  const int2 item = items[it];
-  const int pos = A.sn[item.x].c0 + item.y;
-  const long long r0 = A.run_off[pos];
-  const int total = int(A.run_off[pos + 1] - r0);
+  const int4 R = __ldg(rec + it);
+  const long long r0 = (long long)(unsigned)R.z | ((long long)R.w << 32);
   const cplx* run = A.vals + (long long)c * A.nvals + r0;
-  const int* zi = A.zidx + r0;
-  const cplx* X = A.X + (long long)t * A.nw;
-  const cplx part = gather_dot<4>(run, zi, lane, total, 32, X);
+  const long long base = (long long)t * A.nw;
+  const cplx part = gather_dot<4>(run, A.zidx + r0, lane, R.y, 32, A.X + base);
   const cplx sum = warp_sum(part);
-  if (lane == 0) A.Y[(long long)t * A.nw + pos] = csub(A.B[(long long)t * A.nw + pos], sum);
+  if (lane == 0) A.Y[base + R.x] = csub(A.B[base + R.x], sum);
 }
 
 // separator rows, sub-warp of G lanes per (class, row, member): each group
@@ -269,7 +292,9 @@ template <bool TO_X>
 __global__ void __launch_bounds__(kThreads) k_bwd_pull(SolveArgs A, int ncls, const int2* items,
                                                        int nitem) {
   int c, it, t;
-  if (!decode(A, ncls, (long long)blockIdx.x * blockDim.x + threadIdx.x, nitem, c, it, t)) return;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (!(A.bwd_mm ? decode_mm(A, ncls, idx, nitem, c, it, t) : decode(A, ncls, idx, nitem, c, it, t)))
+    return;
   const int2 item = items[it];
   const DevSn sn = A.sn[item.x];
   const int j = item.y;
@@ -286,7 +311,9 @@ __global__ void __launch_bounds__(kThreads) k_bwd_pull(SolveArgs A, int ncls, co
 __global__ void __launch_bounds__(kThreads) k_bwd_diag(SolveArgs A, int ncls, const int2* items,
                                                        int nitem) {
   int c, it, t;
-  if (!decode(A, ncls, (long long)blockIdx.x * blockDim.x + threadIdx.x, nitem, c, it, t)) return;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (!(A.bwd_mm ? decode_mm(A, ncls, idx, nitem, c, it, t) : decode(A, ncls, idx, nitem, c, it, t)))
+    return;
   const int2 item = items[it];
   const DevSn sn = A.sn[item.x];
   const int j = item.y;
@@ -539,11 +566,11 @@ void launch_solve(const SolveArgs& A, const SolvePlan& P, int ncls, int max_rhs,
     const unsigned gw = grid_for((long long)max_rhs * L.nitem * 32);
     const long long w = (long long)max_rhs * L.nitem;
     switch (L.group) {
-      case 32: k_fwd_pull_warp<<<gw, kThreads, 0, st>>>(A, ncls, L.d_items, L.nitem); break;
+      case 32: k_fwd_pull_warp<<<gw, kThreads, 0, st>>>(A, ncls, L.d_rec, L.nitem); break;
       case 16: k_fwd_pull_sub<16><<<grid_for(w * 16), kThreads, 0, st>>>(A, ncls, L.d_items, L.nitem); break;
       case 8: k_fwd_pull_sub<8><<<grid_for(w * 8), kThreads, 0, st>>>(A, ncls, L.d_items, L.nitem); break;
       case 4: k_fwd_pull_sub<4><<<grid_for(w * 4), kThreads, 0, st>>>(A, ncls, L.d_items, L.nitem); break;
-      default: k_fwd_pull<<<g, kThreads, 0, st>>>(A, ncls, L.d_items, L.nitem); break;
+      default: k_fwd_pull<<<g, kThreads, 0, st>>>(A, ncls, L.d_rec, L.nitem); break;
     }
     if (L.warp_diag)
       k_fwd_diag_warp<<<gw, kThreads, 0, st>>>(A, ncls, L.d_items, L.nitem);
