@@ -63,6 +63,58 @@ __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// Asynchronous 16-byte global -> shared copy (cp.async, L2 only): no register
+// staging, so a CTA can keep thousands of copies in flight.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+// ------------------------------------------------------------ vector layout
+// Per-subdomain vectors (B, X, Y, U, R, C; factor order) are stored member-
+// interleaved per class: element (t, pos) lives at base[t] + pos * str[t], with
+// str[t] = the member count of t's class and base[t] = class offset + member
+// slot. Threads walking the members of one (class, item) touch consecutive
+// addresses; the factor entry they share is one broadcast load.
+struct VMap {
+  const long long* base;  // per RHS t
+  const int* str;         // per RHS t
+  const long long* cbase; // per class c (ncls + 1): storage offset of the class block
+  const int* cptr;        // class membership CSR; slot k of class c is cmem[cptr[c] + k]
+  const int* cmem;
+  int ncls;
+  long long total;        // storage length (= nsub * nw)
+};
+
+// storage index e -> (RHS t, position pos)
+__device__ __forceinline__ void vdecode(const VMap& m, long long e, int& t, int& pos) {
+  int lo = 0, hi = m.ncls - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(m.cbase + mid) <= e) lo = mid; else hi = mid - 1;
+  }
+  const int c0 = __ldg(m.cptr + lo), nm = __ldg(m.cptr + lo + 1) - c0;
+  const long long r = e - __ldg(m.cbase + lo);
+  pos = int(r / nm);
+  t = __ldg(m.cmem + c0 + int(r - (long long)pos * nm));
+}
+
+template <class T>
+struct SVec {  // strided view of one subdomain's vector
+  T* p;
+  int s;
+  __device__ __forceinline__ T& operator[](long long i) const { return p[i * s]; }
+  __device__ __forceinline__ SVec operator+(long long i) const { return {p + i * s, s}; }
+};
+
+template <class T>
+__device__ __forceinline__ SVec<T> vview(T* v, const VMap& m, int t) {
+  return {v + __ldg(m.base + t), __ldg(m.str + t)};
+}
+
 // ------------------------------------------------------------ device tables
 struct DevSn {
   int kind, c0, n, nrows;

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
 #include <chrono>
 #include <complex>
 #include <cstdint>
@@ -88,6 +89,7 @@ struct hddm_engine {
   int2* d_seg = nullptr;
   int* d_zidx = nullptr;
   int* d_bw_ptr = nullptr;
+  std::vector<int> h_bw_ptr;
   BwRow* d_bw = nullptr;
   int* d_perm = nullptr;
   int* d_pinv = nullptr;
@@ -99,6 +101,12 @@ struct hddm_engine {
   int sa_stride = 0;
   double* d_wx = nullptr;
   double* d_wy = nullptr;
+  // per-subdomain vector layout (VMap, dev.cuh): member-interleaved per class
+  long long* d_vbase = nullptr;
+  int* d_vstr = nullptr;
+  long long* d_cbase = nullptr;
+  std::vector<long long> h_vbase;
+  std::vector<int> h_vstr;
   cplx* d_U[3] = {};
   cplx* d_B = nullptr;
   cplx* d_Y = nullptr;
@@ -126,9 +134,12 @@ struct hddm_engine {
   // one CUDA graph per step variant (step 1; s >= 2 by s mod 3), each with a
   // conditional WHILE node running the refinement corrections on demand
   cudaStream_t st2 = nullptr;
-  std::vector<cudaStream_t> cls_st;     // per-class streams for the step graphs
-  std::vector<cudaEvent_t> cls_ev;
-  cudaEvent_t fork_ev = nullptr;
+  struct ForkSet {  // per-tile streams of a forked solve
+    std::vector<cudaStream_t> st;
+    std::vector<cudaEvent_t> ev;
+    cudaEvent_t fork = nullptr;
+  };
+  ForkSet fork_main, fork_body;
   bool per_class_streams = true;
   cudaGraphExec_t step_exec[4] = {};
   int step_kernels = 0;
@@ -187,9 +198,11 @@ struct hddm_engine {
     if (h_scal) cudaFreeHost(h_scal);
     for (auto& g : step_exec)
       if (g) cudaGraphExecDestroy(g);
-    for (auto& x : cls_st) cudaStreamDestroy(x);
-    for (auto& x : cls_ev) cudaEventDestroy(x);
-    if (fork_ev) cudaEventDestroy(fork_ev);
+    for (ForkSet* F : {&fork_main, &fork_body}) {
+      for (auto& x : F->st) cudaStreamDestroy(x);
+      for (auto& x : F->ev) cudaEventDestroy(x);
+      if (F->fork) cudaEventDestroy(F->fork);
+    }
     if (st2) cudaStreamDestroy(st2);
     if (st) cudaStreamDestroy(st);
   }
@@ -198,7 +211,30 @@ struct hddm_engine {
   void factorize();
   void run_probe();
   StepArgs step_args(int s, const cplx* f);
-  SolveArgs solve_args(const cplx* B, cplx* X, cplx* Y);
+  // solve of the RHS t with (flag[t] != 0) == on: B -> X (Y scratch)
+  SolveArgs solve_args(const cplx* B, cplx* X, cplx* Y, const int* flag, int on);
+  void enqueue_solve(const SolveArgs& A, cudaStream_t stream);
+  int* d_zero = nullptr;  // nsub zero flags: every RHS active
+  VMap vmap() const {
+    VMap m;
+    m.base = d_vbase;
+    m.str = d_vstr;
+    m.cbase = d_cbase;
+    m.cptr = d_cls_ptr;
+    m.cmem = d_cls_mem;
+    m.ncls = ncls;
+    m.total = (long long)nsub * nw;
+    return m;
+  }
+  // one subdomain's vector between device storage and a contiguous host array
+  void put_vec(cplx* dv, int t, const cplx* h, cudaStream_t s) {
+    CK(cudaMemcpy2DAsync(dv + h_vbase[t], sizeof(cplx) * h_vstr[t], h, sizeof(cplx), sizeof(cplx), nw,
+                         cudaMemcpyHostToDevice, s));
+  }
+  void get_vec(const cplx* dv, int t, cplx* h, cudaStream_t s) {
+    CK(cudaMemcpy2DAsync(h, sizeof(cplx), dv + h_vbase[t], sizeof(cplx) * h_vstr[t], sizeof(cplx), nw,
+                         cudaMemcpyDeviceToHost, s));
+  }
   CheckArgs check_args(const cplx* Bp, const cplx* X, const int* zc, const int* only);
   RefineArgs refine_args(const cplx* Bp, cplx* X, const int* zc, unsigned long long cond);
   void enqueue_step_front(int s, cudaStream_t stream, unsigned long long cond);
@@ -348,12 +384,15 @@ void hddm_engine::create(const hddm_problem& p) {
           bw.push_back(w);
         }
       }
+      // by first stored column: a column pass stops at the first row beyond it
+      std::stable_sort(bw.begin() + bptr[s], bw.end(),
+                       [](const BwRow& a, const BwRow& b) { return a.first < b.first; });
     }
     bptr[Y.sn.size()] = int(bw.size());
     d_bw_ptr = upload(bptr);
+    h_bw_ptr = bptr;
     d_bw = upload(bw);
   }
-  build_plan();
 
   // ---- per-subdomain data
   std::vector<DevSub> subs(nsub);
@@ -399,6 +438,22 @@ void hddm_engine::create(const hddm_problem& p) {
   d_wy = upload(wy);
   d_cls_ptr = upload(S.cls_ptr);
   d_cls_mem = upload(S.cls_members);
+  {
+    h_vbase.assign(nsub, 0);
+    h_vstr.assign(nsub, 0);
+    std::vector<long long> cb(ncls + 1);
+    for (int c = 0; c <= ncls; ++c) cb[c] = (long long)S.cls_ptr[c] * nw;
+    for (int c = 0; c < ncls; ++c)
+      for (int k = S.cls_ptr[c]; k < S.cls_ptr[c + 1]; ++k) {
+        const int t = S.cls_members[k];
+        h_vbase[t] = cb[c] + (k - S.cls_ptr[c]);
+        h_vstr[t] = S.cls_ptr[c + 1] - S.cls_ptr[c];
+      }
+    d_vbase = upload(h_vbase);
+    d_vstr = upload(h_vstr);
+    d_cbase = upload(cb);
+  }
+  build_plan();
   for (int k = 0; k < 3; ++k) {
     d_U[k] = dalloc<cplx>(size_t(nsub) * nw);
     d_Z[k] = dalloc<int>(nsub);
@@ -407,6 +462,8 @@ void hddm_engine::create(const hddm_problem& p) {
   d_Y = dalloc<cplx>(size_t(nsub) * nw);
   CK(cudaMemsetAsync(d_B, 0, size_t(nsub) * nw * sizeof(cplx), st));
   d_fany = dalloc<int>(nsub);
+  d_zero = dalloc<int>(nsub);
+  CK(cudaMemsetAsync(d_zero, 0, sizeof(int) * nsub, st));
   d_act_ptr = dalloc<int>(ncls + 1);
   d_act_list = dalloc<int>(nsub);
   d_counts = dalloc<long long>(2);
@@ -526,9 +583,71 @@ void hddm_engine::build_plan() {
     if (nd.kind == 0)
       for (int i = 0; i < nd.n; ++i)
         if (i - Y.row_first[nd.drow0 + i] > 6) throw std::runtime_error("leaf band wider than 6");
+  // member tiles (up to 32 members of one class), grouped by member count M:
+  // a group shares every launch (optionally capped at HDDM_GROUP_TILES tiles)
+  std::vector<int> Rs;  // distinct columns-per-CTA of the backward split kernels
+  {
+    std::map<int, std::vector<TileRec>> byM;
+    for (int c = 0; c < ncls; ++c) {
+      const int m = S.cls_ptr[c + 1] - S.cls_ptr[c];
+      for (int k0 = 0; k0 < m; k0 += 32) {
+        TileRec T = {};
+        T.cb = (long long)S.cls_ptr[c] * nw + k0;
+        T.c = c;
+        T.m = m;
+        const int M = std::min(32, m - k0);
+        for (int k = 0; k < 32; ++k) T.t[k] = S.cls_members[S.cls_ptr[c] + k0 + std::min(k, M - 1)];
+        byM[M].push_back(T);
+      }
+    }
+    // 4 tiles per group measured best at config 4 (more, shorter launch chains
+    // overlap better; 1 per group is launch-bound)
+    const char* cap_env = std::getenv("HDDM_GROUP_TILES");
+    const int cap = cap_env ? std::max(1, std::atoi(cap_env)) : 4;
+    for (auto& kv : byM) {
+      const int M = kv.first;
+      if (std::find(Rs.begin(), Rs.end(), 32 / M) == Rs.end()) Rs.push_back(32 / M);
+      for (size_t a = 0; a < kv.second.size(); a += cap) {
+        const size_t b = std::min(kv.second.size(), a + size_t(cap));
+        std::vector<TileRec> part(kv.second.begin() + a, kv.second.begin() + b);
+        TileArg G;
+        G.rec = upload(part);
+        G.ntile = int(part.size());
+        G.M = M;
+        G.E = 1;
+        G.R = 32 / M;
+        for (auto& t : part) {
+          plan.tiles.push_back(t);
+          plan.tile_group.push_back(int(plan.groups.size()));
+        }
+        plan.groups.push_back(G);
+      }
+    }
+  }
+  auto chunks4 = [&](SolveLevel& L, const std::vector<int>& sns) {
+    std::vector<int4> ch;
+    int cw = 0;
+    for (int s : sns)
+      for (int j = 0; j < Y.sn[s].n; j += 32) {
+        const int j1 = std::min(Y.sn[s].n, j + 32);
+        ch.push_back(make_int4(s, j, j1, 0));
+        cw = std::max(cw, j1 - j);
+      }
+    L.nchunk4 = int(ch.size());
+    L.d_chunks4 = upload(ch);
+    L.cw_max = cw;
+  };
+  plan.staged = std::getenv("HDDM_NO_STAGE") == nullptr;
+  if (const char* v = std::getenv("HDDM_CTA_RUN")) plan.cta_run = std::atol(v);
+  if (const char* v = std::getenv("HDDM_CTA_DIAG")) plan.cta_diag = std::atol(v);
   plan.fwd_leaf = level(leaves);
   plan.bwd_leaf = level(leaves);
   plan.bwd_leafcol = level(leafcols);
+  {
+    std::vector<int> ls;
+    for (const int2& l : leaves) ls.push_back(l.x);
+    chunks4(plan.bwd_leafcol, ls);
+  }
   for (int h = 1; h <= Y.max_height; ++h) {
     std::vector<int2> v;
     for (int s = 0; s < nsn; ++s)
@@ -536,67 +655,47 @@ void hddm_engine::build_plan() {
         for (int i = 0; i < Y.sn[s].n; ++i) v.push_back(make_int2(s, i));
     if (v.empty()) continue;
     SolveLevel L = level(v);
-    {
-      std::vector<int4> rec(v.size());
-      for (size_t k = 0; k < v.size(); ++k) {
-        const int pos = Y.sn[v[k].x].c0 + v[k].y;
-        const long long ro = Y.run_off[pos];
-        rec[k] = make_int4(pos, int(Y.run_off[pos + 1] - ro), int(ro & 0xffffffffLL), int(ro >> 32));
-      }
-      L.d_rec = upload(rec);
+    std::vector<int4> rec(v.size());
+    long tot = 0, dtot = 0;
+    for (size_t k = 0; k < v.size(); ++k) {
+      const int pos = Y.sn[v[k].x].c0 + v[k].y;
+      const long long ro = Y.run_off[pos];
+      rec[k] = make_int4(pos, int(Y.run_off[pos + 1] - ro), int(ro & 0xffffffffLL), int(ro >> 32));
+      tot += rec[k].y;
+      dtot += v[k].y;
     }
-    long tot = 0;
-    for (const int2& it : v) tot += Y.run_off[Y.sn[it.x].c0 + it.y + 1] - Y.run_off[Y.sn[it.x].c0 + it.y];
-    L.warp_rows = tot > 128L * long(v.size());  // average run longer than 4 warp strides
-    const long avg = tot / long(v.size());
-    L.group = avg > 128 ? 32 : 1;  // sub-warp groups measured slower than thread-per-row
-    if (const char* g = std::getenv("HDDM_FWD_GROUP")) L.group = std::atoi(g);
-    {
-      int nmax = 0;
-      std::vector<int2> seps;
-      for (const int2& it : v)
-        if (it.y == 0) seps.push_back(make_int2(it.x, 0));
-      for (const int2& sp : seps) nmax = std::max(nmax, Y.sn[sp.x].n);
-      if (nmax <= 32 && std::getenv("HDDM_SMALL")) {  // measured slower: opt-in
-        L.small_g = nmax <= 8 ? 8 : nmax <= 16 ? 16 : 32;
-        L.nsmall = int(seps.size());
-        L.d_small = upload(seps);
-      }
-    }
-    long dsum = 0;
-    for (const int2& it : v) dsum += it.y;
-    L.warp_diag = dsum > 48L * long(v.size());   // average inverse row longer than 48
+    L.d_rec = upload(rec);
+    L.avg_run = tot / long(v.size());
+    L.avg_diag = dtot / long(v.size());
     plan.fwd.push_back(L);
   }
+  const char* env_sr = std::getenv("HDDM_SPLIT_ROWS");
+  const char* env_sd = std::getenv("HDDM_SPLIT_DIAG");
   for (int d = 0; d <= Y.max_depth; ++d) {
-    std::vector<int2> v, ch;
-    long rows = 0, cols = 0, nmax = 0;
+    std::vector<int2> v;
+    std::vector<int> sns;
+    long rows = 0, nmax = 0;
     for (int s = 0; s < nsn; ++s)
       if (Y.sn[s].kind == 1 && Y.sn[s].depth == d) {
+        sns.push_back(s);
         for (int i = 0; i < Y.sn[s].n; ++i) v.push_back(make_int2(s, i));
-        for (int i = 0; i < Y.sn[s].n; i += 32) ch.push_back(make_int2(s, i));
-        long nr = 0;
-        for (int b = Y.sn[s].blk0; b < Y.sn[s].blk0 + Y.sn[s].nblk; ++b) nr += Y.blk[b].nr;
-        rows += nr * Y.sn[s].n;
-        cols += Y.sn[s].n;
+        rows += h_bw_ptr[s + 1] - h_bw_ptr[s];
         nmax = std::max<long>(nmax, Y.sn[s].n);
       }
     if (v.empty()) continue;
     SolveLevel L = level(v);
-    if (nmax <= 32 && std::getenv("HDDM_SMALL")) {  // measured slower: opt-in
-      std::vector<int2> seps;
-      for (const int2& it : v)
-        if (it.y == 0) seps.push_back(make_int2(it.x, 0));
-      L.small_g = nmax <= 8 ? 8 : nmax <= 16 ? 16 : 32;
-      L.nsmall = int(seps.size());
-      L.d_small = upload(seps);
-    }
-    L.warp_rows = rows > 64L * cols;  // more than 64 rows per column
-    L.warp_diag = nmax > 48;
-    if (L.warp_rows || L.warp_diag) {
-      L.nchunk = int(ch.size());
-      L.d_chunks = upload(ch);
-    }
+    chunks4(L, sns);
+    L.split_rows = rows > 64L * long(sns.size());  // long row lists
+    L.split_diag = nmax > 48;
+    if (env_sr) L.split_rows = std::atoi(env_sr) != 0;
+    if (env_sd) L.split_diag = std::atoi(env_sd) != 0;
+    if (L.split_rows || L.split_diag)
+      for (int Rg : Rs) {
+        std::vector<int2> g;
+        for (int s : sns)
+          for (int i = 0; i < Y.sn[s].n; i += Rg) g.push_back(make_int2(s, i));
+        L.groups[Rg] = std::make_pair(int(g.size()), upload(g));
+      }
     plan.bwd.push_back(L);
   }
 }
@@ -690,7 +789,7 @@ void hddm_engine::factorize() {
   factor_ms = now_ms() - t0;
 }
 
-SolveArgs hddm_engine::solve_args(const cplx* Bp, cplx* X, cplx* Yp) {
+SolveArgs hddm_engine::solve_args(const cplx* Bp, cplx* X, cplx* Yp, const int* flag, int on) {
   SolveArgs A;
   A.sn = d_sn;
   A.blk = d_blk;
@@ -704,17 +803,14 @@ SolveArgs hddm_engine::solve_args(const cplx* Bp, cplx* X, cplx* Yp) {
   A.bw = d_bw;
   A.vals = d_vals;
   A.nvals = Y.nvals;
-  A.act_ptr = d_act_ptr;
-  A.act_list = d_act_list;
+  A.flag = flag;
+  A.flag_on = on;
   A.B = Bp;
   A.X = X;
   A.Y = Yp;
+  A.vm = vmap();
   A.nw = nw;
   A.nring = Y.nring;
-  static const int mm = std::getenv("HDDM_MEMBER_MAJOR") ? std::atoi(std::getenv("HDDM_MEMBER_MAJOR")) : 0;
-  A.member_major = mm;
-  static const int bmm = std::getenv("HDDM_BWD_MM") ? std::atoi(std::getenv("HDDM_BWD_MM")) : 0;
-  A.bwd_mm = bmm;
   return A;
 }
 
@@ -738,14 +834,14 @@ void hddm_engine::run_probe() {
     zc[t] = 0;
     aptr[c] = c;
     alist[c] = t;
-    CK(cudaMemcpyAsync(d_B + size_t(t) * nw, bfo.data(), nw * sizeof(cplx), cudaMemcpyHostToDevice, st));
+    put_vec(d_B, t, bfo.data(), st);
   }
   aptr[ncls] = ncls;
   CK(cudaMemcpyAsync(d_Z[0], zc.data(), sizeof(int) * nsub, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_act_ptr, aptr.data(), sizeof(int) * (ncls + 1), cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_act_list, alist.data(), sizeof(int) * ncls, cudaMemcpyHostToDevice, st));
   CK(cudaStreamSynchronize(st));
-  launch_solve(solve_args(d_B, d_U[0], d_Y), plan, ncls, ncls, st);
+  enqueue_solve(solve_args(d_B, d_U[0], d_Y, d_Z[0], 0), st);
   CK(cudaMemsetAsync(d_refine, 0, sizeof(int), st));
   CK(cudaMemsetAsync(d_maxrel, 0, sizeof(double), st));
   host_refine(d_B, d_U[0], d_Z[0]);
@@ -794,6 +890,7 @@ StepArgs hddm_engine::step_args(int s, const cplx* f) {
   A.zc = d_Z[s % 3];
   A.zp1 = d_Z[(s + 2) % 3];
   A.zp2 = d_Z[(s + 1) % 3];
+  A.vm = vmap();
   A.B = d_B;
   A.Ucur = d_U[s % 3];
   A.Up1 = d_U[(s + 2) % 3];
@@ -843,6 +940,7 @@ CheckArgs hddm_engine::check_args(const cplx* Bp, const cplx* X, const int* zc,
   C.zc = zc;
   C.only = only;
   C.nsub = nsub;
+  C.vm = vmap();
   C.B = Bp;
   C.X = X;
   C.part = d_part_chk;
@@ -871,6 +969,7 @@ RefineArgs hddm_engine::refine_args(const cplx* Bp, cplx* X, const int* zc,
   R.perm = d_perm;
   R.pinv = d_pinv;
   R.zc = zc;
+  R.vm = vmap();
   R.B = Bp;
   R.X = X;
   R.R = d_R;
@@ -896,31 +995,39 @@ void hddm_engine::enqueue_step_front(int s, cudaStream_t stream, unsigned long l
   const StepArgs A = step_args(s, d_f);
   launch_flags(A, ncls, stream);
   launch_gather(A, stream);
-  if (per_class_streams && stream == st && ncls > 1) {
-    // fork: every class runs its level chain on its own stream, so its
-    // vectors stay L2-resident between consecutive levels; join afterwards
-    if (cls_st.empty()) {
-      cls_st.resize(ncls);
-      cls_ev.resize(ncls);
-      for (int c = 0; c < ncls; ++c) {
-        CK(cudaStreamCreateWithFlags(&cls_st[c], cudaStreamNonBlocking));
-        CK(cudaEventCreateWithFlags(&cls_ev[c], cudaEventDisableTiming));
-      }
-      CK(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
-    }
-    CK(cudaEventRecord(fork_ev, stream));
-    const SolveArgs SA = solve_args(d_B, A.Ucur, d_Y);
-    for (int c = 0; c < ncls; ++c) {
-      CK(cudaStreamWaitEvent(cls_st[c], fork_ev, 0));
-      launch_solve_class(SA, plan, c, S.cls_ptr[c + 1] - S.cls_ptr[c], cls_st[c]);
-      CK(cudaEventRecord(cls_ev[c], cls_st[c]));
-    }
-    for (int c = 0; c < ncls; ++c) CK(cudaStreamWaitEvent(stream, cls_ev[c], 0));
-  } else {
-    launch_solve(solve_args(d_B, A.Ucur, d_Y), plan, ncls, nsub, stream);
-  }
+  enqueue_solve(solve_args(d_B, A.Ucur, d_Y, A.zc, 0), stream);
   launch_check(check_args(d_B, A.Ucur, A.zc, nullptr), stream);
   launch_refine_init(refine_args(d_B, A.Ucur, A.zc, cond), stream);
+}
+
+// The batched solve on `stream`. On the engine stream, every class runs its
+// level chain on its own forked stream (classes overlap; a class's vectors stay
+// L2-resident between its consecutive levels), joined afterwards.
+void hddm_engine::enqueue_solve(const SolveArgs& SA, cudaStream_t stream) {
+  const int nt = int(plan.groups.size());
+  if (!per_class_streams || nt == 1 || (stream != st && stream != st2)) {
+    for (int g = 0; g < nt; ++g) launch_solve_group(SA, plan, g, stream);
+    return;
+  }
+  // one stream set per origin stream: st (step front) and st2 (the refinement
+  // body, captured while st's capture is open)
+  ForkSet& F = stream == st ? fork_main : fork_body;
+  if (F.st.empty()) {
+    F.st.resize(nt);
+    F.ev.resize(nt);
+    for (int g = 0; g < nt; ++g) {
+      CK(cudaStreamCreateWithFlags(&F.st[g], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&F.ev[g], cudaEventDisableTiming));
+    }
+    CK(cudaEventCreateWithFlags(&F.fork, cudaEventDisableTiming));
+  }
+  CK(cudaEventRecord(F.fork, stream));
+  for (int g = 0; g < nt; ++g) {
+    CK(cudaStreamWaitEvent(F.st[g], F.fork, 0));
+    launch_solve_group(SA, plan, g, F.st[g]);
+    CK(cudaEventRecord(F.ev[g], F.st[g]));
+  }
+  for (int g = 0; g < nt; ++g) CK(cudaStreamWaitEvent(stream, F.ev[g], 0));
 }
 
 // One correction pass of refine for every RHS still above 1e-11.
@@ -928,7 +1035,7 @@ void hddm_engine::enqueue_refine_body(int s, cudaStream_t stream, unsigned long 
   const StepArgs A = step_args(s, d_f);
   const RefineArgs R = refine_args(d_B, A.Ucur, A.zc, cond);
   launch_refine_prep(R, stream);
-  launch_solve(solve_args(d_R, d_C, d_Y), plan, ncls, nsub, stream);
+  enqueue_solve(solve_args(d_R, d_C, d_Y, d_need, 1), stream);
   launch_refine_apply(R, stream);
   launch_check_partials(check_args(d_B, A.Ucur, A.zc, d_need), stream);
   launch_refine_decide(R, stream);
@@ -1011,7 +1118,7 @@ void hddm_engine::host_refine(const cplx* Bp, cplx* X, const int* zc) {
     CK(cudaStreamSynchronize(st));
     if (!any) break;
     launch_refine_prep(R, st);
-    launch_solve(solve_args(d_R, d_C, d_Y), plan, ncls, nsub, st);
+    enqueue_solve(solve_args(d_R, d_C, d_Y, d_need, 1), st);
     launch_refine_apply(R, st);
     launch_check_partials(check_args(Bp, X, zc, d_need), st);
     launch_refine_decide(R, st);
@@ -1417,8 +1524,8 @@ int hddm_tap_subdomain(hddm_engine* e, int t, double* rhs, double* u, int* activ
     const int s = e->last_step;
     std::vector<cplx> b(e->nw), x(e->nw);
     int z = 1;
-    CK(cudaMemcpyAsync(b.data(), e->d_B + size_t(t) * e->nw, e->nw * sizeof(cplx), cudaMemcpyDeviceToHost, e->st));
-    CK(cudaMemcpyAsync(x.data(), e->d_U[s % 3] + size_t(t) * e->nw, e->nw * sizeof(cplx), cudaMemcpyDeviceToHost, e->st));
+    e->get_vec(e->d_B, t, b.data(), e->st);
+    e->get_vec(e->d_U[s % 3], t, x.data(), e->st);
     CK(cudaMemcpyAsync(&z, e->d_Z[s % 3] + t, sizeof(int), cudaMemcpyDeviceToHost, e->st));
     CK(cudaStreamSynchronize(e->st));
     for (int k = 0; k < e->nw; ++k) {
@@ -1445,15 +1552,15 @@ int hddm_class_solve(hddm_engine* e, int c, const double* b, double* x, double* 
     zc[t] = 0;
     for (int k = c + 1; k <= e->ncls; ++k) aptr[k] = 1;
     cudaStream_t st = e->st;
-    CK(cudaMemcpyAsync(e->d_B + size_t(t) * e->nw, bfo.data(), e->nw * sizeof(cplx), cudaMemcpyHostToDevice, st));
+    e->put_vec(e->d_B, t, bfo.data(), st);
     CK(cudaMemcpyAsync(e->d_Z[0], zc.data(), sizeof(int) * e->nsub, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(e->d_act_ptr, aptr.data(), sizeof(int) * (e->ncls + 1), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(e->d_act_list, alist.data(), sizeof(int), cudaMemcpyHostToDevice, st));
-    launch_solve(e->solve_args(e->d_B, e->d_U[0], e->d_Y), e->plan, e->ncls, 1, st);
+    e->enqueue_solve(e->solve_args(e->d_B, e->d_U[0], e->d_Y, e->d_Z[0], 0), st);
     e->host_refine(e->d_B, e->d_U[0], e->d_Z[0]);
     std::vector<cplx> xf(e->nw);
     double rel = 0;
-    CK(cudaMemcpyAsync(xf.data(), e->d_U[0] + size_t(t) * e->nw, e->nw * sizeof(cplx), cudaMemcpyDeviceToHost, st));
+    e->get_vec(e->d_U[0], t, xf.data(), st);
     CK(cudaMemcpyAsync(&rel, e->d_relcur + t, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     for (int k = 0; k < e->nw; ++k) {
@@ -1493,16 +1600,15 @@ long long hddm_launch_count(const hddm_engine* e) { return e->launches; }
 
 int hddm_time_solve(hddm_engine* e, int reps, double* ms_per_solve) {
   return guarded(e, [&] {
-    // steady state: every subdomain active, right-hand sides of the last step
-    std::vector<int> aptr(e->ncls + 1), alist(e->nsub);
-    for (int c = 0; c <= e->ncls; ++c) aptr[c] = e->S.cls_ptr[c];
-    for (int k = 0; k < e->nsub; ++k) alist[k] = e->S.cls_members[k];
+    // steady state: every subdomain active, right-hand sides of the last step,
+    // the step graphs' per-class stream structure
     cudaStream_t st = e->st;
-    CK(cudaMemcpyAsync(e->d_act_ptr, aptr.data(), sizeof(int) * (e->ncls + 1), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(e->d_act_list, alist.data(), sizeof(int) * e->nsub, cudaMemcpyHostToDevice, st));
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    launch_solve(e->solve_args(e->d_B, e->d_C, e->d_Y), e->plan, e->ncls, e->nsub, st);
+    set_solve_skip(std::getenv("HDDM_SKIP") ? std::atoi(std::getenv("HDDM_SKIP")) : 0,
+                   std::getenv("HDDM_ONLY_TILE") ? std::atoi(std::getenv("HDDM_ONLY_TILE")) : -1);
+    e->enqueue_solve(e->solve_args(e->d_B, e->d_C, e->d_Y, e->d_zero, 0), st);
+    set_solve_skip(0, -1);
     CK(cudaStreamEndCapture(st, &g));
     cudaGraphExec_t x;
     CK(cudaGraphInstantiate(&x, g, 0));

@@ -1,6 +1,8 @@
 // Kernel argument blocks and launcher prototypes (host <-> .cu glue).
 #pragma once
 
+#include <map>
+#include <utility>
 #include <vector>
 
 #include "dev.cuh"
@@ -21,31 +23,48 @@ struct SolveArgs {
   const BwRow* bw;
   const cplx* vals;    // ncls x nvals
   long long nvals;
-  const int* act_ptr;  // CSR over classes of right-hand-side ids
-  const int* act_list;
-  const cplx* B;       // right-hand sides (factor order), stride nw
-  cplx* X;             // solutions (factor order), stride nw
-  cplx* Y;             // scratch, stride nw
+  const int* flag;     // per RHS t: active iff (flag[t] != 0) == flag_on
+  int flag_on;
+  const cplx* B;       // right-hand sides (factor order), layout vm
+  cplx* X;             // solutions (factor order), layout vm
+  cplx* Y;             // scratch, layout vm
+  VMap vm;
   int nw, nring;
-  int member_major;  // thread order: 0 class/item/member, 1 class/member/item
-  int bwd_mm;        // backward kernels member-major
 };
 
-// One level of the level-synchronous sweeps: a flat list of output items
-// (supernode, row/column index) or (leaf, 0) that are independent given the
-// previous levels. Threads are laid out class-major, then item, then member.
+// A member tile: up to 32 members of one class.
+struct TileRec {
+  long long cb;  // storage offset of (position 0, first member of the tile)
+  int c;         // class
+  int m;         // class member count = vector stride
+  int t[32];     // RHS id of each tile member
+};
+
+// A tile group: tiles with the same member count M share every launch; the lane
+// shape (R items x E element lanes x M members per warp) is set per launch.
+struct TileArg {
+  const TileRec* rec;
+  int ntile;
+  int M, E, R;
+};
+
+// One level of the level-synchronous sweeps: output items that are independent
+// given the previous levels -- rows (supernode, row) / leaves (leaf, 0) forward,
+// columns (supernode, column) backward.
 struct SolveLevel {
   int nitem = 0;
   int2* d_items = nullptr;
-  int4* d_rec = nullptr;   // forward: (position, run length, run offset lo, hi) per item
-  bool warp_rows = false;  // long pulls: forward warp per row / backward split rows
-  int group = 1;           // forward pull: lanes per row (1, 4, 8, 16, 32)
-  bool warp_diag = false;  // large separators: split the dense-inverse products
-  int small_g = 0;         // >0: fused pull+diagonal, this many lanes per separator
-  int nsmall = 0;          // (separator, 0) items of the fused kernels
-  int2* d_small = nullptr;
-  int nchunk = 0;          // backward split variants: (supernode, 32-column chunk) items
-  int2* d_chunks = nullptr;
+  int4* d_rec = nullptr;    // forward rows: (position, run length, run offset lo, hi)
+  long avg_run = 0;         // forward: mean incoming run length
+  long avg_diag = 0;        // forward: mean dense-inverse row length
+  bool split_rows = false;  // backward pull: a CTA of 8 warps splits long row lists
+  bool split_diag = false;  // backward diagonal: a CTA splits the inverse columns
+  // backward split kernels: per columns-per-CTA R, the groups (supernode, first column)
+  std::map<int, std::pair<int, int2*>> groups;
+  // backward staged kernels: column chunks (supernode, j0, j1, -) of <= 32 columns
+  int nchunk4 = 0;
+  int4* d_chunks4 = nullptr;
+  int cw_max = 0;
 };
 
 struct SolvePlan {
@@ -54,14 +73,20 @@ struct SolvePlan {
   std::vector<SolveLevel> bwd;         // separator columns by depth (pull, then diag)
   SolveLevel bwd_leafcol;              // leaf columns: w = Dinv z - B^T x
   SolveLevel bwd_leaf;                 // leaves: band back-substitution
+  std::vector<TileArg> groups;         // tile groups (E, R set per launch)
+  std::vector<TileRec> tiles;          // host copy of every tile
+  std::vector<int> tile_group;         // group of each tile
+  bool staged = true;                  // backward pulls through shared memory
+  // forward: CTA per row above these mean lengths (measured slower at config 4:
+  // off by default, HDDM_CTA_RUN / HDDM_CTA_DIAG)
+  long cta_run = 1L << 40;
+  long cta_diag = 1L << 40;
 };
 
-// max_rhs bounds the number of active right-hand sides over all classes
-void launch_solve(const SolveArgs& A, const SolvePlan& P, int ncls, int max_rhs,
-                  cudaStream_t st);
-int solve_launch_count(const SolvePlan& P);
-void launch_solve_class(const SolveArgs& A, const SolvePlan& P, int c, int members,
-                        cudaStream_t st);
+// one tile group's full solve (all levels) on one stream
+void launch_solve_group(const SolveArgs& A, const SolvePlan& P, int g, cudaStream_t st);
+int solve_launch_count(const SolvePlan& P);  // kernels of one solve over all tiles
+void set_solve_skip(int mask, int only_tile);  // profiling aid (hddm_time_solve only)
 
 // ------------------------------------------------------------------ factor
 struct FactorArgs {
@@ -106,6 +131,7 @@ struct StepArgs {
   int* zc;               // flags of this step (1 = zero/skipped)
   const int* zp1;
   const int* zp2;
+  VMap vm;               // layout of B and the U vectors
   cplx* B;               // rhs (factor order)
   cplx* Ucur;            // this step's solutions (factor order)
   const cplx* Up1;       // previous step
@@ -141,6 +167,7 @@ struct CheckArgs {
   const int* zc;      // per RHS: 1 = inactive
   const int* only;    // if set: process RHS t only when only[t] != 0 (refinement re-checks)
   int nsub;
+  VMap vm;
   const cplx* B;
   const cplx* X;
   double* part;      // nsub x nchunk x 2
@@ -165,6 +192,7 @@ struct RefineArgs {
   const int* perm;
   const int* pinv;
   const int* zc;
+  VMap vm;            // layout of B, X, R, C
   const cplx* B;
   cplx* X;
   cplx* R;            // residual vectors (correction right-hand sides)

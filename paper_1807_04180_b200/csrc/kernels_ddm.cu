@@ -142,11 +142,12 @@ __device__ __forceinline__ bool in_patch(int d, const DevSub& T, int wnx, int wn
 //      identical for every window): B = J * (f_owned - sum_d L_t(beta_d v_d))
 //      over the in-range, non-zero-flagged sources in kGatherOrder.
 __global__ void __launch_bounds__(256) k_rhs_base(StepArgs A) {
-  const int t = blockIdx.y;
+  // storage order: the members of a class at one position are adjacent
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= A.vm.total) return;
+  int t, pos;
+  vdecode(A.vm, e, t, pos);
   if (A.zc[t]) return;
-  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
-  if (pos >= A.nw) return;
-  cplx* Bt = A.B + (long long)t * A.nw;
   cplx v = cmk(0, 0);
   if (A.step == 1) {
     const int node = A.perm[pos];
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(256) k_rhs_base(StepArgs A) {
       }
     }
   }
-  Bt[pos] = v;
+  A.B[e] = v;
 }
 
 __global__ void __launch_bounds__(256) k_rhs_transfer(StepArgs A) {
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(256) k_rhs_transfer(StepArgs A) {
     const bool corner = d >= 4;
     if ((corner ? A.zp2 : A.zp1)[src]) continue;
     any = true;
-    const cplx* V = (corner ? A.Up2 : A.Up1) + (long long)src * A.nw;
+    const SVec<const cplx> V = vview(corner ? A.Up2 : A.Up1, A.vm, src);
     // source-local coordinates of the target node: windows are offset by whole cores
     const int sp = lp - di * A.mcx, sq = lq - dj * A.mcy;
     const bool fromL = d == 1 || d == 5 || d == 7, fromR = d == 0 || d == 4 || d == 6;
@@ -226,12 +227,11 @@ __global__ void __launch_bounds__(256) k_rhs_transfer(StepArgs A) {
     tt = csub(tt, cmul(cS, csub(uc, w5[4])));
     val = csub(val, cadd(cdiv(tt, jac), cscale(uc, k2)));
   }
-  if (any) A.B[(long long)t * A.nw + A.pinv[node]] = cmul(jac, val);
+  if (any) vview(A.B, A.vm, t)[A.pinv[node]] = cmul(jac, val);
 }
 
 void launch_gather(const StepArgs& A, cudaStream_t st) {
-  dim3 g((A.nw + 255) / 256, A.nsub);
-  k_rhs_base<<<g, 256, 0, st>>>(A);
+  k_rhs_base<<<unsigned((A.vm.total + 255) / 256), 256, 0, st>>>(A);
   dim3 g2((A.npatch + 255) / 256, A.nsub);
   k_rhs_transfer<<<g2, 256, 0, st>>>(A);
 }
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(256) k_accumulate(StepArgs A) {
       if (wy == 0.0) continue;
       const double w = A.wx[(long long)t * A.wnx + (P - T.wx0)] * wy;
       if (w == 0.0) continue;
-      const cplx u = A.Ucur[(long long)t * A.nw + A.pinv[(Q - T.wy0) * A.wnx + (P - T.wx0)]];
+      const cplx u = vview((const cplx*)A.Ucur, A.vm, t)[A.pinv[(Q - T.wy0) * A.wnx + (P - T.wx0)]];
       acc.x = __dadd_rn(acc.x, __dmul_rn(w, u.x));
       acc.y = __dadd_rn(acc.y, __dmul_rn(w, u.y));
       touched = true;
@@ -273,7 +273,8 @@ void launch_accumulate(const StepArgs& A, cudaStream_t st) {
 // ------------------------------------------------------------ residual check
 // (A x)_pos for the J-scaled assembled matrix of subdomain t's window
 // (discretize.cpp:98-160): identity ring rows, ring columns dropped.
-__device__ __forceinline__ cplx ax_row(const cplx* __restrict__ X, int pos, int wnx, int wny,
+template <class XV>
+__device__ __forceinline__ cplx ax_row(XV X, int pos, int wnx, int wny,
                                        int gnx, double ih2, const DevSub& T, const cplx* sa,
                                        const double* k2g, const int* perm, const int* pinv) {
   const int node = perm[pos];
@@ -304,8 +305,8 @@ __global__ void __launch_bounds__(256) k_check(CheckArgs A) {
   const bool act = A.only ? A.only[t] != 0 : !A.zc[t];
   double r2 = 0, b2 = 0;
   if (act) {
-    const cplx* X = A.X + (long long)t * A.nw;
-    const cplx* Bv = A.B + (long long)t * A.nw;
+    const SVec<const cplx> X = vview(A.X, A.vm, t);
+    const SVec<const cplx> Bv = vview(A.B, A.vm, t);
     const DevSub T = A.sub[t];
     const cplx* sa = A.sa + (long long)t * A.sa_stride;
     const cplx* a1n = sa;
@@ -420,19 +421,20 @@ __global__ void __launch_bounds__(256) k_refine_resid(RefineArgs R) {
   const int pos = blockIdx.x * blockDim.x + threadIdx.x;
   if (pos >= R.nw) return;
   const DevSub T = R.sub[t];
-  const cplx* X = R.X + (long long)t * R.nw;
+  const SVec<const cplx> X = vview((const cplx*)R.X, R.vm, t);
   const cplx ax = ax_row(X, pos, R.wnx, R.wny, R.gnx, R.ih2, T, R.sa + (long long)t * R.sa_stride,
                          R.k2, R.perm, R.pinv);
-  R.R[(long long)t * R.nw + pos] = csub(R.B[(long long)t * R.nw + pos], ax);
+  const long long p = (X.p - R.X) + (long long)pos * X.s;
+  R.R[p] = csub(R.B[p], ax);
 }
 
 // X += C for the refining RHS
 __global__ void __launch_bounds__(256) k_refine_apply(RefineArgs R) {
-  const int t = blockIdx.y;
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= R.vm.total) return;
+  int t, pos;
+  vdecode(R.vm, p, t, pos);
   if (!R.need[t]) return;
-  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
-  if (pos >= R.nw) return;
-  const long long p = (long long)t * R.nw + pos;
   R.X[p] = cadd(R.X[p], R.C[p]);
 }
 
@@ -474,13 +476,12 @@ __global__ void k_refine_decide(RefineArgs R) {
 }
 
 __global__ void __launch_bounds__(256) k_refine_undo(RefineArgs R) {
-  const int t = blockIdx.y;
-  if (!R.undo[t]) return;
-  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
-  if (pos >= R.nw) return;
-  const long long p = (long long)t * R.nw + pos;
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= R.vm.total) return;
+  int t, pos;
+  vdecode(R.vm, p, t, pos);
+  if (!R.undo[t]) return;  // flag cleared by the next init
   R.X[p] = csub(R.X[p], R.C[p]);
-  if (pos == 0) {}  // flag cleared by the next init
 }
 
 void launch_refine_init(const RefineArgs& R, cudaStream_t st) {
@@ -492,15 +493,13 @@ void launch_refine_prep(const RefineArgs& R, cudaStream_t st) {
   k_refine_resid<<<g, 256, 0, st>>>(R);
 }
 void launch_refine_apply(const RefineArgs& R, cudaStream_t st) {
-  dim3 g((R.nw + 255) / 256, R.nsub);
-  k_refine_apply<<<g, 256, 0, st>>>(R);
+  k_refine_apply<<<unsigned((R.vm.total + 255) / 256), 256, 0, st>>>(R);
 }
 void launch_refine_decide(const RefineArgs& R, cudaStream_t st) {
   k_refine_decide<<<1, 256, 0, st>>>(R);
 }
 void launch_refine_undo(const RefineArgs& R, cudaStream_t st) {
-  dim3 g((R.nw + 255) / 256, R.nsub);
-  k_refine_undo<<<g, 256, 0, st>>>(R);
+  k_refine_undo<<<unsigned((R.vm.total + 255) / 256), 256, 0, st>>>(R);
 }
 
 // ------------------------------------------------------------ global stencil

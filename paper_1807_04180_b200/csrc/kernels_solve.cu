@@ -1,25 +1,34 @@
 // Batched multi-RHS supernodal triangular solves (the per-step hot path that
 // replaces Factorization::solve -> solve_raw, proj/src/sparse.cpp:244-266).
 //
-// Level-synchronous over the nested-dissection tree: every kernel handles one
-// level for ALL classes and ALL active member right-hand sides at once, one
-// thread per (class, output item, member). Threads are ordered class-major,
-// then item, then member, so the members of a class sharing a factor entry sit
-// in the same warp (one load, broadcast), and consecutive output columns of a
-// supernode read consecutive factor entries (coalesced). Each thread runs one
-// short sequential dot product; hundreds of thousands of independent threads
-// per level keep the memory system busy.
+// Level-synchronous over the nested-dissection tree. The right-hand sides of a
+// factor class are stored member-interleaved (VMap, dev.cuh), and the work of a
+// class is cut into MEMBER TILES of up to 32 members; every kernel launch
+// serves one tile (its descriptor travels in the kernel parameters, so a warp
+// needs no setup loads). A warp's 32 lanes are split as R x E x M:
+//   k = lane % M          member of the tile (consecutive lanes: consecutive
+//                         members -> contiguous vector entries, one factor
+//                         entry broadcast to all of them),
+//   e = lane / M % E      element lane within one output (E > 1: the lanes
+//                         stride a long run, partial sums reduced by shuffles),
+//   r = lane / (E M)      output item (R items per warp).
+// The host picks E and R per level and tile: singleton classes stride their
+// runs with E lanes (coalesced factor / index / vector reads), multi-member
+// tiles keep E = 1 deep in the tree (lanes over members already coalesce) and
+// widen E near the root where runs are long and items few.
 //
-//   forward, leaves:      z_leaf = L_leaf^{-1} b_leaf              (band)
+//   forward, leaves:      z_leaf = L_leaf^{-1} b_leaf              (band, registers)
 //   forward, separators:  y_r = b_r - (incoming run of row r) . z   (pull)
 //                         z_s = Linv_s y_s                         (dense inverse)
-//   backward, separators: w_j = z_j / D_j - sum_r L[r][j] x_r       (pull)
-//                         x_s = Linv_s^T w_s
+//   backward, separators: w_j = z_j / D_j - sum_r L[r][j] x_r       (pull, rows sorted
+//                         x_s = Linv_s^T w_s                        by first column)
 //   backward, leaves:     the same pull per leaf column, then a band
 //                         back-substitution per leaf
 //   ring (identity rows): x = b
 // Every output has one writer and a fixed summation order: deterministic.
-// Vectors are in factor order; RHS index = subdomain id, stride nw.
+#include <algorithm>
+#include <cstdlib>
+
 #include "dev.cuh"
 #include "kernels.cuh"
 
@@ -28,52 +37,62 @@ namespace hddm {
 namespace {
 
 constexpr int kThreads = 256;
+#ifndef HDDM_UF
+#define HDDM_UF 4
+#endif
+#ifndef HDDM_UB
+#define HDDM_UB 4
+#endif
+constexpr int kUF = HDDM_UF;  // forward gathers in flight per lane
+constexpr int kUB = HDDM_UB;  // backward rows in flight per lane
+constexpr unsigned kFull = 0xffffffffu;
 
-// thread -> (class c, item, RHS t); false past the end of the work list
-__device__ __forceinline__ bool decode(const SolveArgs& A, int ncls, long long idx, int nitem,
-                                       int& c, int& item, int& t) {
-  // act_ptr may be a per-class view (ap[0] != 0): offsets are relative to ap[0]
-  const int* ap = A.act_ptr;
-  const int a0 = ap[0];
-  if (idx >= (long long)(ap[ncls] - a0) * nitem) return false;
-  int lo = 0, hi = ncls - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if ((long long)(ap[mid] - a0) * nitem <= idx) lo = mid; else hi = mid - 1;
-  }
-  c = lo;
-  const int m = ap[c + 1] - ap[c];
-  const long long r = idx - (long long)(ap[c] - a0) * nitem;
-  if (A.member_major) {  // consecutive threads: consecutive items of one RHS
-    const int k = int(r / nitem);
-    item = int(r - (long long)k * nitem);
-    t = A.act_list[ap[c] + k];
-  } else {               // consecutive threads: the members of one item
-    item = int(r / m);
-    t = A.act_list[ap[c] + int(r - (long long)item * m)];
-  }
-  return true;
+// one lane of a tile-group launch: warp w serves tile w / wpt of the group
+// (wpt = warps per tile for this level), items (w % wpt) * R + r
+struct TL {
+  int r, e, k;    // item within the warp, element lane, member
+  int c, m;       // class, member count (vector stride)
+  long long cb;   // storage offset of (position 0, member k of the tile)
+  long long it;   // item index of this lane
+  bool act;       // lane maps to an active right-hand side
+};
+
+__device__ __forceinline__ void tile_fill(const SolveArgs& A, const TileArg& T, int ti, bool in,
+                                          TL& L) {
+  const TileRec* rec = T.rec + (in ? ti : 0);
+  L.c = rec->c;
+  L.m = rec->m;
+  L.cb = rec->cb + L.k;
+  const int t = rec->t[L.k];
+  L.act = in && (A.flag[t] != 0) == (A.flag_on != 0);
 }
 
-// member-major decode: consecutive threads walk consecutive items of ONE right-
-// hand side (backward sweeps: a warp covers consecutive columns, so the
-// ancestor value x_r is a broadcast and the factor row a coalesced read)
-__device__ __forceinline__ bool decode_mm(const SolveArgs& A, int ncls, long long idx, int nitem,
-                                          int& c, int& item, int& t) {
-  const int* ap = A.act_ptr;
-  const int a0 = ap[0];
-  if (idx >= (long long)(ap[ncls] - a0) * nitem) return false;
-  int lo = 0, hi = ncls - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if ((long long)(ap[mid] - a0) * nitem <= idx) lo = mid; else hi = mid - 1;
+__device__ __forceinline__ TL tile_lane(const SolveArgs& A, const TileArg& T, int nitem) {
+  const int lane = threadIdx.x & 31;
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long wpt = (nitem + T.R - 1) / T.R;
+  const int ti = int(w / wpt);
+  TL L;
+  L.k = lane % T.M;
+  L.e = (lane / T.M) % T.E;
+  L.r = lane / (T.M * T.E);
+  L.it = (w - (long long)ti * wpt) * T.R + L.r;
+  tile_fill(A, T, ti, ti < T.ntile && L.r < T.R && L.it < nitem, L);
+  return L;
+}
+
+__device__ __forceinline__ long long vat(const TL& L, int pos) {
+  return L.cb + (long long)pos * L.m;
+}
+
+// sum over the E element lanes of each (item, member); result valid at e == 0
+__device__ __forceinline__ cplx tile_reduce(cplx v, const TileArg& T, const TL& L) {
+  for (int step = 1; step < T.E; step <<= 1) {
+    const double ox = __shfl_down_sync(kFull, v.x, step * T.M);
+    const double oy = __shfl_down_sync(kFull, v.y, step * T.M);
+    if ((L.e & (2 * step - 1)) == 0 && L.e + step < T.E) v = cadd(v, cmk(ox, oy));
   }
-  c = lo;
-  const long long r = idx - (long long)(ap[c] - a0) * nitem;
-  const int k = int(r / nitem);
-  item = int(r - (long long)k * nitem);
-  t = A.act_list[ap[c] + k];
-  return true;
+  return v;
 }
 
 __device__ __forceinline__ void csub_mul(cplx& acc, cplx l, cplx x) {
@@ -81,12 +100,13 @@ __device__ __forceinline__ void csub_mul(cplx& acc, cplx l, cplx x) {
   acc.y -= l.x * x.y + l.y * x.x;
 }
 
-// sum_{q = start, start+step, ... < n} L[q] * X[zi[q]], software-pipelined:
-// the next batch's factor values and source indices are in flight while the
-// current batch's gathers are consumed.
+// sum_{q = start, start+step, ... < n} L[q] * X[zi[q] * m]; factor values and
+// source indices of the next batch are in flight while the current batch's
+// vector entries are consumed
 template <int U>
 __device__ __forceinline__ cplx gather_dot(const cplx* __restrict__ L, const int* __restrict__ zi,
-                                           int start, int n, int step, const cplx* __restrict__ X) {
+                                           int start, int n, int step, const cplx* __restrict__ X,
+                                           int m) {
   cplx acc0 = cmk(0, 0), acc1 = cmk(0, 0);
   cplx l[U];
   int ix[U];
@@ -100,7 +120,7 @@ __device__ __forceinline__ cplx gather_dot(const cplx* __restrict__ L, const int
   for (int q0 = start; q0 < n; q0 += U * step) {
     cplx x[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) x[u] = ix[u] >= 0 ? X[ix[u]] : cmk(0, 0);
+    for (int u = 0; u < U; ++u) x[u] = ix[u] >= 0 ? X[(long long)ix[u] * m] : cmk(0, 0);
     cplx ln[U];
     int ixn[U];
 #pragma unroll
@@ -121,12 +141,22 @@ __device__ __forceinline__ cplx gather_dot(const cplx* __restrict__ L, const int
   return cadd(acc0, acc1);
 }
 
-// sum over backward rows of L[r][j] * X[dst r] for column j, pipelined the
-// same way (row descriptors of the next batch in flight)
+// rows of a backward list (sorted by first stored column) that touch column j
+__device__ __forceinline__ int rows_upto(const BwRow* rows, int nr, int j) {
+  int lo = 0, hi = nr;  // first index with first > j
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (rows[mid].first <= j) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// sum over rows k = start, start+step, ... < nr of L[r][j] * X[dpos_r * m],
+// row descriptors of the next batch in flight
 template <int U>
 __device__ __forceinline__ cplx bw_gather(const cplx* __restrict__ vals, const BwRow* __restrict__ rows,
                                           int start, int nr, int step, int j,
-                                          const cplx* __restrict__ X) {
+                                          const cplx* __restrict__ X, int m) {
   cplx acc0 = cmk(0, 0), acc1 = cmk(0, 0);
   BwRow d[U];
 #pragma unroll
@@ -140,7 +170,7 @@ __device__ __forceinline__ cplx bw_gather(const cplx* __restrict__ vals, const B
     for (int u = 0; u < U; ++u) {
       const bool ok = j >= d[u].first;
       l[u] = ok ? ldf(vals + d[u].off + (j - d[u].first)) : cmk(0, 0);
-      x[u] = ok ? X[d[u].dpos] : cmk(0, 0);
+      x[u] = ok ? X[(long long)d[u].dpos * m] : cmk(0, 0);
     }
     BwRow dn[U];
 #pragma unroll
@@ -156,40 +186,42 @@ __device__ __forceinline__ cplx bw_gather(const cplx* __restrict__ vals, const B
   return cadd(acc0, acc1);
 }
 
+
 }  // namespace
 
-// identity ring rows: x = b (thread per (class, ring position, member))
-__global__ void __launch_bounds__(kThreads) k_ring(SolveArgs A, int ncls) {
-  int c, it, t;
-  if (!decode(A, ncls, (long long)blockIdx.x * blockDim.x + threadIdx.x, A.nring, c, it, t)) return;
-  const long long p = (long long)t * A.nw + it;
+// identity ring rows: x = b (thread per (position, member))
+__global__ void __launch_bounds__(kThreads) k_ring(SolveArgs A, TileArg T) {
+  const TL L = tile_lane(A, T, A.nring);
+  if (!L.act) return;
+  const long long p = vat(L, int(L.it));
   A.X[p] = A.B[p];
 }
 
 // leaves, forward: z_i = b_i - sum_{q in [first_i, i)} L[i][q] z_q. The band is
-// at most kBand wide (checked at setup), so the last kBand values live in a
-// register window.
+// at most kBand wide (checked at setup): the last kBand values live in registers.
+// Thread per (leaf, member): T.E == 1, R = 32 / M leaves per warp.
 constexpr int kBand = 6;
 
-__global__ void __launch_bounds__(kThreads) k_fwd_leaf(SolveArgs A, int ncls, const int2* items,
+__global__ void __launch_bounds__(kThreads) k_fwd_leaf(SolveArgs A, TileArg T, const int2* items,
                                                        int nitem) {
-  int c, it, t;
-  if (!decode(A, ncls, (long long)blockIdx.x * blockDim.x + threadIdx.x, nitem, c, it, t)) return;
+  const TL L = tile_lane(A, T, nitem);
+  const long long it = L.it;
+  if (!L.act) return;
   const DevSn sn = A.sn[items[it].x];
-  const cplx* vals = A.vals + (long long)c * A.nvals;
-  const cplx* b = A.B + (long long)t * A.nw + sn.c0;
-  cplx* x = A.X + (long long)t * A.nw + sn.c0;
+  const cplx* vals = A.vals + (long long)L.c * A.nvals;
+  const SVec<const cplx> b{A.B + vat(L, sn.c0), L.m};
+  const SVec<cplx> x{A.X + vat(L, sn.c0), L.m};
   cplx win[kBand + 1];  // win[d] = z_{i-d}
 #pragma unroll
   for (int d = 0; d <= kBand; ++d) win[d] = cmk(0, 0);
   for (int i = 0; i < sn.n; ++i) {
     const int rt = sn.drow0 + i;
     const int first = A.row_first[rt];
-    const cplx* L = vals + A.row_off[rt] - first;  // L[q] for q in [first, i)
+    const cplx* Lr = vals + A.row_off[rt] - first;  // L[q] for q in [first, i)
     cplx acc = b[i];
 #pragma unroll
     for (int d = 1; d <= kBand; ++d)
-      if (i - d >= first) csub_mul(acc, ldf(L + i - d), win[d]);
+      if (i - d >= first) csub_mul(acc, ldf(Lr + i - d), win[d]);
 #pragma unroll
     for (int d = kBand; d >= 2; --d) win[d] = win[d - 1];
     win[1] = acc;
@@ -197,128 +229,152 @@ __global__ void __launch_bounds__(kThreads) k_fwd_leaf(SolveArgs A, int ncls, co
   }
 }
 
-// separator rows, forward pull: Y[r] = B[r] - run(r) . X[src] (thread per row).
-// rec[item] = (position, run length, run offset lo, hi): one load of setup.
-__global__ void __launch_bounds__(kThreads) k_fwd_pull(SolveArgs A, int ncls, const int4* rec,
+// separator rows, forward pull: Y[r] = B[r] - run(r) . X[src].
+// rec[item] = (position, run length, run offset lo, hi).
+__global__ void __launch_bounds__(kThreads) k_fwd_pull(SolveArgs A, TileArg T, const int4* rec,
                                                        int nitem) {
-  int c, it, t;
-  if (!decode(A, ncls, (long long)blockIdx.x * blockDim.x + threadIdx.x, nitem, c, it, t)) return;
-  const int4 R = __ldg(rec + it);
-  const long long r0 = (long long)(unsigned)R.z | ((long long)R.w << 32);
-  const cplx* run = A.vals + (long long)c * A.nvals + r0;
-  const long long base = (long long)t * A.nw;
-  const cplx s = gather_dot<4>(run, A.zidx + r0, 0, R.y, 1, A.X + base);
-  A.Y[base + R.x] = csub(A.B[base + R.x], s);
-}
-
-// separator rows with long runs (top levels): one WARP per (class, row,
-// member); lanes stride the run (coalesced), zidx gives each element's source.
-__global__ void __launch_bounds__(kThreads) k_fwd_pull_warp(SolveArgs A, int ncls,
-                                                            const int4* rec, int nitem) {
-  int c, it, t;
-  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (!decode(A, ncls, w, nitem, c, it, t)) return;
-  const int4 R = __ldg(rec + it);
-  const long long r0 = (long long)(unsigned)R.z | ((long long)R.w << 32);
-  const cplx* run = A.vals + (long long)c * A.nvals + r0;
-  const long long base = (long long)t * A.nw;
-  const cplx part = gather_dot<4>(run, A.zidx + r0, lane, R.y, 32, A.X + base);
-  const cplx sum = warp_sum(part);
-  if (lane == 0) A.Y[base + R.x] = csub(A.B[base + R.x], sum);
-}
-
-// separator rows, sub-warp of G lanes per (class, row, member): each group
-// reads its run in G-wide coalesced chunks; a 32-lane warp serves 32/G rows.
-template <int G>
-__global__ void __launch_bounds__(kThreads) k_fwd_pull_sub(SolveArgs A, int ncls,
-                                                           const int2* items, int nitem) {
-  int c, it, t;
-  const long long gid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / G;
-  const int sl = threadIdx.x & (G - 1);
-  const bool live = decode(A, ncls, gid, nitem, c, it, t);
+  const TL L = tile_lane(A, T, nitem);
+  const long long it = L.it;
+  const bool live = L.act;
+  int4 R = make_int4(0, 0, 0, 0);
   cplx acc = cmk(0, 0);
-  int pos = 0;
   if (live) {
-    const int2 item = items[it];
-    pos = A.sn[item.x].c0 + item.y;
-    const long long r0 = A.run_off[pos];
-    const int total = int(A.run_off[pos + 1] - r0);
-    const cplx* run = A.vals + (long long)c * A.nvals + r0;
-    const int* zi = A.zidx + r0;
-    const cplx* X = A.X + (long long)t * A.nw;
-    cplx acc1 = cmk(0, 0);
-    int q = sl;
-    for (; q + G < total; q += 2 * G) {
-      const cplx l0 = ldf(run + q), l1 = ldf(run + q + G);
-      const int i0 = __ldg(zi + q), i1 = __ldg(zi + q + G);
-      cfma(acc, l0, X[i0]);
-      cfma(acc1, l1, X[i1]);
-    }
-    if (q < total) cfma(acc, ldf(run + q), X[__ldg(zi + q)]);
-    acc = cadd(acc, acc1);
+    R = __ldg(rec + it);
+    const long long r0 = (long long)(unsigned)R.z | ((long long)R.w << 32);
+    acc = gather_dot<kUF>(A.vals + (long long)L.c * A.nvals + r0, A.zidx + r0, L.e, R.y, T.E,
+                        A.X + L.cb, L.m);
   }
-#pragma unroll
-  for (int m = G / 2; m > 0; m >>= 1) acc = cadd(acc, shfl_xor(acc, m));
-  if (live && sl == 0) A.Y[(long long)t * A.nw + pos] = csub(A.B[(long long)t * A.nw + pos], acc);
+  if (T.E > 1) acc = tile_reduce(acc, T, L);
+  if (live && L.e == 0) {
+    const long long p = vat(L, R.x);
+    A.Y[p] = csub(A.B[p], acc);
+  }
+}
+
+// Long runs (top levels): a CTA of 8 warps per (tile, row); warp w strides the
+// run with its E element lanes at offset w * E, partial sums combined in fixed
+// warp order. DIAG: the dense-inverse row instead of the incoming run.
+template <bool DIAG>
+__global__ void __launch_bounds__(kThreads) k_fwd_cta(SolveArgs A, TileArg T, const int4* rec,
+                                                      const int2* items, int nitem) {
+  __shared__ cplx part[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ti = blockIdx.x / nitem;
+  const int it = blockIdx.x - ti * nitem;
+  TL L;
+  L.k = lane % T.M;
+  L.e = (lane / T.M) % T.E;
+  L.r = lane / (T.M * T.E);
+  L.it = it;
+  tile_fill(A, T, ti, L.r == 0, L);
+  cplx acc = cmk(0, 0);
+  long long out = 0;
+  if (L.act) {
+    if (DIAG) {
+      const int2 item = items[it];
+      const DevSn sn = A.sn[item.x];
+      const int i = item.y;
+      const SVec<const cplx> y{A.Y + vat(L, sn.c0), L.m};
+      const cplx* row = A.vals + (long long)L.c * A.nvals + sn.diag_off + (long long)i * (i - 1) / 2;
+      cplx a2 = cmk(0, 0);
+      const int st = 8 * T.E;
+      int j = warp * T.E + L.e;
+      for (; j + st < i; j += 2 * st) {
+        const cplx l0 = ldf(row + j), l1 = ldf(row + j + st);
+        const cplx v0 = y[j], v1 = y[j + st];
+        cfma(acc, l0, v0);
+        cfma(a2, l1, v1);
+      }
+      if (j < i) cfma(acc, ldf(row + j), y[j]);
+      acc = cadd(acc, a2);
+      out = vat(L, sn.c0 + i);
+    } else {
+      const int4 R = __ldg(rec + it);
+      const long long r0 = (long long)(unsigned)R.z | ((long long)R.w << 32);
+      acc = gather_dot<kUF>(A.vals + (long long)L.c * A.nvals + r0, A.zidx + r0,
+                            warp * T.E + L.e, R.y, 8 * T.E, A.X + L.cb, L.m);
+      out = vat(L, R.x);
+    }
+  }
+  if (T.E > 1) acc = tile_reduce(acc, T, L);
+  part[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && L.act && L.e == 0) {
+    cplx sum = part[0][lane];
+    for (int w = 1; w < 8; ++w) sum = cadd(sum, part[w][lane]);
+    if (DIAG)
+      A.X[out] = cadd(A.Y[out], sum);
+    else
+      A.Y[out] = csub(A.B[out], sum);
+  }
 }
 
 // separator rows, forward diagonal: X[i] = Y[i] + sum_{j<i} Linv[i][j] Y[j]
-__global__ void __launch_bounds__(kThreads) k_fwd_diag(SolveArgs A, int ncls, const int2* items,
+__global__ void __launch_bounds__(kThreads) k_fwd_diag(SolveArgs A, TileArg T, const int2* items,
                                                        int nitem) {
-  int c, it, t;
-  if (!decode(A, ncls, (long long)blockIdx.x * blockDim.x + threadIdx.x, nitem, c, it, t)) return;
-  const int2 item = items[it];
-  const DevSn sn = A.sn[item.x];
-  const int i = item.y;
-  const cplx* row = A.vals + (long long)c * A.nvals + sn.diag_off + (long long)i * (i - 1) / 2;
-  const cplx* y = A.Y + (long long)t * A.nw + sn.c0;
-  cplx acc = y[i];
-  int j = 0;
-  for (; j + 4 <= i; j += 4) {
-    const cplx l0 = ldf(row + j), l1 = ldf(row + j + 1), l2 = ldf(row + j + 2), l3 = ldf(row + j + 3);
-    cfma(acc, l0, y[j]);
-    cfma(acc, l1, y[j + 1]);
-    cfma(acc, l2, y[j + 2]);
-    cfma(acc, l3, y[j + 3]);
+  const TL L = tile_lane(A, T, nitem);
+  const long long it = L.it;
+  const bool live = L.act;
+  int2 item = make_int2(0, 0);
+  long long y0 = 0;
+  cplx acc = cmk(0, 0), acc2 = cmk(0, 0);
+  if (live) {
+    item = items[it];
+    const DevSn sn = A.sn[item.x];
+    const int i = item.y;
+    y0 = vat(L, sn.c0);
+    const SVec<const cplx> y{A.Y + y0, L.m};
+    const cplx* row = A.vals + (long long)L.c * A.nvals + sn.diag_off + (long long)i * (i - 1) / 2;
+    int j = L.e;
+    for (; j + T.E < i; j += 2 * T.E) {
+      const cplx l0 = ldf(row + j), l1 = ldf(row + j + T.E);
+      const cplx v0 = y[j], v1 = y[j + T.E];
+      cfma(acc, l0, v0);
+      cfma(acc2, l1, v1);
+    }
+    if (j < i) cfma(acc, ldf(row + j), y[j]);
   }
-  for (; j < i; ++j) cfma(acc, ldf(row + j), y[j]);
-  A.X[(long long)t * A.nw + sn.c0 + i] = acc;
+  acc = cadd(acc, acc2);
+  if (T.E > 1) acc = tile_reduce(acc, T, L);
+  if (live && L.e == 0) {
+    const long long p = y0 + (long long)item.y * L.m;
+    A.X[p] = cadd(A.Y[p], acc);
+  }
 }
 
-// backward pull for column j of supernode s: w = Dinv[j] X[j] - sum_rows L[r][j] X[dst r]
-// (dst = scratch target: Y for separators, X in place for leaves)
+// backward pull, thread per (column, member) (T.E == 1; items are columns):
+// w_j = Dinv[j] X[j] - sum_rows L[r][j] X[dst r] into Y (in place into X for leaf
+// columns). Rows are sorted by first stored column: column j walks only the
+// rows that reach it.
 template <bool TO_X>
-__global__ void __launch_bounds__(kThreads) k_bwd_pull(SolveArgs A, int ncls, const int2* items,
+__global__ void __launch_bounds__(kThreads) k_bwd_pull(SolveArgs A, TileArg T, const int2* items,
                                                        int nitem) {
-  int c, it, t;
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (!(A.bwd_mm ? decode_mm(A, ncls, idx, nitem, c, it, t) : decode(A, ncls, idx, nitem, c, it, t)))
-    return;
+  const TL L = tile_lane(A, T, nitem);
+  const long long it = L.it;
+  if (!L.act) return;
   const int2 item = items[it];
   const DevSn sn = A.sn[item.x];
   const int j = item.y;
-  const cplx* vals = A.vals + (long long)c * A.nvals;
-  const cplx* X = A.X + (long long)t * A.nw;
-  cplx acc = cmul(ldg(vals + sn.dinv_off + j), X[sn.c0 + j]);
+  const cplx* vals = A.vals + (long long)L.c * A.nvals;
   const BwRow* rows = A.bw + A.bw_ptr[item.x];
-  const int nr = A.bw_ptr[item.x + 1] - A.bw_ptr[item.x];
-  acc = csub(acc, bw_gather<4>(vals, rows, 0, nr, 1, j, X));
-  (TO_X ? A.X : A.Y)[(long long)t * A.nw + sn.c0 + j] = acc;
+  const int nr = rows_upto(rows, A.bw_ptr[item.x + 1] - A.bw_ptr[item.x], j);
+  const cplx acc = bw_gather<kUB>(vals, rows, 0, nr, 1, j, A.X + L.cb, L.m);
+  const long long p = vat(L, sn.c0 + j);
+  (TO_X ? A.X : A.Y)[p] = csub(cmul(ldg(vals + sn.dinv_off + j), A.X[p]), acc);
 }
 
 // separator columns, backward diagonal: X[j] = Y[j] + sum_{i>j} Linv[i][j] Y[i]
-__global__ void __launch_bounds__(kThreads) k_bwd_diag(SolveArgs A, int ncls, const int2* items,
+// (thread per (column, member))
+__global__ void __launch_bounds__(kThreads) k_bwd_diag(SolveArgs A, TileArg T, const int2* items,
                                                        int nitem) {
-  int c, it, t;
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (!(A.bwd_mm ? decode_mm(A, ncls, idx, nitem, c, it, t) : decode(A, ncls, idx, nitem, c, it, t)))
-    return;
+  const TL L = tile_lane(A, T, nitem);
+  const long long it = L.it;
+  if (!L.act) return;
   const int2 item = items[it];
   const DevSn sn = A.sn[item.x];
   const int j = item.y;
-  const cplx* Linv = A.vals + (long long)c * A.nvals + sn.diag_off;
-  const cplx* y = A.Y + (long long)t * A.nw + sn.c0;
+  const cplx* Linv = A.vals + (long long)L.c * A.nvals + sn.diag_off;
+  const SVec<const cplx> y{A.Y + vat(L, sn.c0), L.m};
   cplx acc = y[j], acc2 = cmk(0, 0);
   int i = j + 1;
   for (; i + 4 <= sn.n; i += 4) {
@@ -333,19 +389,174 @@ __global__ void __launch_bounds__(kThreads) k_bwd_diag(SolveArgs A, int ncls, co
     cfma(acc2, l3, y3);
   }
   for (; i < sn.n; ++i) cfma(acc, ldf(Linv + (long long)i * (i - 1) / 2 + j), y[i]);
-  A.X[(long long)t * A.nw + sn.c0 + j] = cadd(acc, acc2);
+  A.X[vat(L, sn.c0 + j)] = cadd(acc, acc2);
+}
+
+// backward, CTA per (column group): lanes cover R = 32 / M columns x M members,
+// the 8 warps split the inner range, partial sums combined in fixed warp order
+// (top levels: few columns, long row lists / inverse columns). items: the
+// group's first column.
+template <bool DIAG>
+__global__ void __launch_bounds__(kThreads) k_bwd_split(SolveArgs A, TileArg T, const int2* items,
+                                                        int nitem) {
+  __shared__ cplx part[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ti = blockIdx.x / nitem;  // CTA per (tile, column group)
+  TL L;
+  L.k = lane % T.M;
+  L.e = 0;
+  L.r = lane / T.M;
+  L.it = 0;
+  tile_fill(A, T, ti, L.r < T.R, L);
+  const int2 item = items[blockIdx.x - ti * nitem];
+  const DevSn sn = A.sn[item.x];
+  const int j = item.y + L.r;
+  const bool ok = L.act && j < sn.n;
+  const cplx* vals = A.vals + (long long)L.c * A.nvals;
+  cplx acc = cmk(0, 0);
+  if (ok) {
+    if (DIAG) {
+      const cplx* Linv = vals + sn.diag_off;
+      const SVec<const cplx> y{A.Y + vat(L, sn.c0), L.m};
+      for (int i = j + 1 + warp; i < sn.n; i += 8)
+        cfma(acc, ldf(Linv + (long long)i * (i - 1) / 2 + j), y[i]);
+    } else {
+      const BwRow* rows = A.bw + A.bw_ptr[item.x];
+      const int nr = rows_upto(rows, A.bw_ptr[item.x + 1] - A.bw_ptr[item.x], j);
+      acc = bw_gather<kUB>(vals, rows, warp, nr, 8, j, A.X + L.cb, L.m);
+    }
+  }
+  part[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && ok) {
+    cplx sum = part[0][lane];
+    for (int w = 1; w < 8; ++w) sum = cadd(sum, part[w][lane]);
+    const long long p = vat(L, sn.c0 + j);
+    if (DIAG)
+      A.X[p] = cadd(A.Y[p], sum);
+    else
+      A.Y[p] = csub(cmul(ldg(vals + sn.dinv_off + j), A.X[p]), sum);
+  }
+}
+
+// backward pull, staged through shared memory. CTA per (tile, column chunk
+// [j0, j1) of supernode s). The rows reaching the chunk (a prefix of the list
+// sorted by first column) are processed RC at a time: their descriptors, the
+// tile members' x values (M contiguous per row) and the rows' factor entries
+// for the chunk columns (a dense RC x CW tile, zero left of each row's first
+// column) are copied with cp.async -- no registers held per load, one wait per
+// row chunk -- then every (column, member) pair accumulates from shared memory.
+// Pairs below the CTA size split the rows S ways (fixed-order combine).
+// w_j = Dinv[j] X[j] - sum_rows L[r][j] X[dst r] into Y (X for leaf columns).
+constexpr int kStageThreads = 128;
+
+template <bool TO_X>
+__global__ void __launch_bounds__(kStageThreads) k_bwd_stage(SolveArgs A, TileArg T,
+                                                             const int4* chunks, int nchunk,
+                                                             int RC, int CWmax) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int ti = blockIdx.x / nchunk;
+  const int4 ch = chunks[blockIdx.x - ti * nchunk];  // (supernode, j0, j1, -)
+  const TileRec* rec = T.rec + ti;
+  const int M = T.M, m = rec->m;
+  const long long cb = rec->cb;
+  const int tid = threadIdx.x;
+  {  // a tile without any active member does nothing (uniform over the CTA)
+    const bool a = tid < M && (A.flag[rec->t[tid]] != 0) == (A.flag_on != 0);
+    if (!__syncthreads_or(a)) return;
+  }
+  const DevSn sn = A.sn[ch.x];
+  const int j0 = ch.y, CW = ch.z - ch.y;
+  const BwRow* rows = A.bw + A.bw_ptr[ch.x];
+  const int nre = rows_upto(rows, A.bw_ptr[ch.x + 1] - A.bw_ptr[ch.x], ch.z - 1);
+  const cplx* vals = A.vals + (long long)rec->c * A.nvals;
+  cplx* xs = reinterpret_cast<cplx*>(smem);            // [RC][M]
+  cplx* ls = xs + (size_t)RC * M;                        // [RC][CW]
+  BwRow* rd = reinterpret_cast<BwRow*>(ls + (size_t)RC * CWmax);  // [RC]
+  cplx* red = reinterpret_cast<cplx*>(rd + RC);          // [kStageThreads] split partials
+  const int P = CW * M;                                  // (column, member) pairs
+  const int S = P >= kStageThreads ? 1 : kStageThreads / P;  // row splits
+  const int pp = tid % P, sp = tid / P;  // split mode: pair, row split
+  constexpr int kMaxQ = 8;  // pairs per thread (P <= kMaxQ * 128)
+  cplx acc[kMaxQ];
+#pragma unroll
+  for (int q = 0; q < kMaxQ; ++q) acc[q] = cmk(0, 0);
+  for (int k0 = 0; k0 < nre; k0 += RC) {
+    const int kc = min(RC, nre - k0);
+    for (int kk = tid; kk < kc; kk += kStageThreads) rd[kk] = rows[k0 + kk];
+    __syncthreads();
+    for (int e = tid; e < kc * M; e += kStageThreads) {
+      const int kk = e / M, mm = e - kk * M;
+      cp_async16(xs + e, A.X + cb + (long long)rd[kk].dpos * m + mm);
+    }
+    for (int e = tid; e < kc * CW; e += kStageThreads) {
+      const int kk = e / CW, j = j0 + (e - kk * CW);
+      const BwRow d = rd[kk];
+      if (j >= d.first)
+        cp_async16(ls + e, vals + d.off + (j - d.first));
+      else
+        ls[e] = cmk(0, 0);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    if (S == 1) {
+#pragma unroll
+      for (int q = 0; q < kMaxQ; ++q) {
+        const int p = tid + q * kStageThreads;
+        if (p < P) {
+          const int jj = p / M, mm = p - jj * M;
+          cplx a = acc[q], a2 = cmk(0, 0);
+          int kk = 0;
+          for (; kk + 1 < kc; kk += 2) {
+            cfma(a, ls[kk * CW + jj], xs[kk * M + mm]);
+            cfma(a2, ls[(kk + 1) * CW + jj], xs[(kk + 1) * M + mm]);
+          }
+          if (kk < kc) cfma(a, ls[kk * CW + jj], xs[kk * M + mm]);
+          acc[q] = cadd(a, a2);
+        }
+      }
+    } else if (sp < S) {
+      const int jj = pp / M, mm = pp - jj * M;
+      cplx a = acc[0];
+      for (int kk = sp; kk < kc; kk += S) cfma(a, ls[kk * CW + jj], xs[kk * M + mm]);
+      acc[0] = a;
+    }
+    __syncthreads();
+  }
+  if (S > 1) {  // combine the row splits in fixed order
+    red[tid] = acc[0];
+    __syncthreads();
+    if (tid < P) {
+      cplx a = red[tid];
+      for (int k = 1; k < S; ++k) a = cadd(a, red[tid + k * P]);
+      acc[0] = a;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kMaxQ; ++q) {
+    const int p = tid + q * kStageThreads;
+    if (p < P && (S == 1 || q == 0)) {
+      const int jj = p / M, mm = p - jj * M;
+      if ((A.flag[rec->t[mm]] != 0) == (A.flag_on != 0)) {
+        const int j = j0 + jj;
+        const long long a = cb + (long long)(sn.c0 + j) * m + mm;
+        (TO_X ? A.X : A.Y)[a] = csub(cmul(ldg(vals + sn.dinv_off + j), A.X[a]), acc[q]);
+      }
+    }
+  }
 }
 
 // leaves, backward band back-substitution on w (held in X): for i = n-1..0:
 // x_i = w_i; w_q -= L[i][q] x_i for q in [first_i, i). Register window of the
-// next kBand pending w values.
-__global__ void __launch_bounds__(kThreads) k_bwd_leaf(SolveArgs A, int ncls, const int2* items,
+// next kBand pending w values. Thread per (leaf, member).
+__global__ void __launch_bounds__(kThreads) k_bwd_leaf(SolveArgs A, TileArg T, const int2* items,
                                                        int nitem) {
-  int c, it, t;
-  if (!decode(A, ncls, (long long)blockIdx.x * blockDim.x + threadIdx.x, nitem, c, it, t)) return;
+  const TL L = tile_lane(A, T, nitem);
+  const long long it = L.it;
+  if (!L.act) return;
   const DevSn sn = A.sn[items[it].x];
-  const cplx* vals = A.vals + (long long)c * A.nvals;
-  cplx* x = A.X + (long long)t * A.nw + sn.c0;
+  const cplx* vals = A.vals + (long long)L.c * A.nvals;
+  const SVec<cplx> x{A.X + vat(L, sn.c0), L.m};
   const int n = sn.n;
   cplx w[kBand + 1];  // w[d] = pending w_{i-d}
 #pragma unroll
@@ -355,258 +566,126 @@ __global__ void __launch_bounds__(kThreads) k_bwd_leaf(SolveArgs A, int ncls, co
     x[i] = xi;
     const int rt = sn.drow0 + i;
     const int first = A.row_first[rt];
-    const cplx* L = vals + A.row_off[rt] - first;
+    const cplx* Lr = vals + A.row_off[rt] - first;
 #pragma unroll
     for (int d = 1; d <= kBand; ++d)
-      if (i - d >= first) csub_mul(w[d], ldf(L + i - d), xi);
+      if (i - d >= first) csub_mul(w[d], ldf(Lr + i - d), xi);
 #pragma unroll
     for (int d = 0; d < kBand; ++d) w[d] = w[d + 1];
     w[kBand] = (i - 1 - kBand >= 0) ? x[i - 1 - kBand] : cmk(0, 0);
   }
 }
 
-// ---------------------------------------------------------- fused small separators
-// Separators with n <= G lanes (deep levels): a group of G lanes per
-// (class, separator, member) does the pull of its rows/columns and then the
-// dense-inverse product through shuffles within the group -- one kernel per
-// level, no scratch round trip. items: (separator, 0).
-template <int G>
-__global__ void __launch_bounds__(kThreads) k_fwd_small(SolveArgs A, int ncls, const int2* items,
-                                                        int nitem) {
-  int c, it, t;
-  const long long gid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / G;
-  const int l = threadIdx.x & (G - 1);
-  const bool live = decode(A, ncls, gid, nitem, c, it, t);
-  const DevSn sn = A.sn[live ? items[it].x : 0];
-  const bool row = live && l < sn.n;
-  const cplx* vals = A.vals + (long long)(live ? c : 0) * A.nvals;
-  cplx y = cmk(0, 0);
-  if (row) {
-    const int pos = sn.c0 + l;
-    const cplx* run = vals + A.run_off[pos];
-    const cplx* X = A.X + (long long)t * A.nw;
-    y = A.B[(long long)t * A.nw + pos];
-    for (int e = A.seg_ptr[pos]; e < A.seg_ptr[pos + 1]; ++e) {
-      const int2 sg = A.seg[e];
-      const cplx* xs = X + sg.y;
-      int j = 0;
-      for (; j + 4 <= sg.x; j += 4) {
-        const cplx l0 = ldf(run + j), l1 = ldf(run + j + 1), l2 = ldf(run + j + 2), l3 = ldf(run + j + 3);
-        const cplx x0 = xs[j], x1 = xs[j + 1], x2 = xs[j + 2], x3 = xs[j + 3];
-        csub_mul(y, l0, x0);
-        csub_mul(y, l1, x1);
-        csub_mul(y, l2, x2);
-        csub_mul(y, l3, x3);
-      }
-      for (; j < sg.x; ++j) csub_mul(y, ldf(run + j), xs[j]);
-      run += sg.x;
-    }
-  }
-  // z_l = y_l + sum_{j<l} Linv[l][j] y_j (y_j broadcast within the group)
-  const cplx* Lrow = vals + sn.diag_off + (long long)l * (l - 1) / 2;
-  cplx z = y;
-  const int n = live ? sn.n : 0;
-  for (int j = 0; j + 1 < n; ++j) {
-    const cplx yj = cmk(__shfl_sync(0xffffffffu, y.x, j, G), __shfl_sync(0xffffffffu, y.y, j, G));
-    if (row && j < l) cfma(z, ldf(Lrow + j), yj);
-  }
-  if (row) A.X[(long long)t * A.nw + sn.c0 + l] = z;
-}
-
-template <int G>
-__global__ void __launch_bounds__(kThreads) k_bwd_small(SolveArgs A, int ncls, const int2* items,
-                                                        int nitem) {
-  int c, it, t;
-  const long long gid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / G;
-  const int j = threadIdx.x & (G - 1);
-  const bool live = decode(A, ncls, gid, nitem, c, it, t);
-  const int sid = live ? items[it].x : 0;
-  const DevSn sn = A.sn[sid];
-  const bool col = live && j < sn.n;
-  const cplx* vals = A.vals + (long long)(live ? c : 0) * A.nvals;
-  cplx w = cmk(0, 0);
-  if (col) {
-    const cplx* X = A.X + (long long)t * A.nw;
-    w = cmul(ldg(vals + sn.dinv_off + j), X[sn.c0 + j]);
-    const BwRow* rows = A.bw + A.bw_ptr[sid];
-    const int nr = A.bw_ptr[sid + 1] - A.bw_ptr[sid];
-    int k = 0;
-    for (; k + 4 <= nr; k += 4) {
-      BwRow d[4];
-      cplx lv[4], xv[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) d[u] = rows[k + u];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const bool ok = j >= d[u].first;
-        lv[u] = ok ? ldf(vals + d[u].off + (j - d[u].first)) : cmk(0, 0);
-        xv[u] = ok ? X[d[u].dpos] : cmk(0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) csub_mul(w, lv[u], xv[u]);
-    }
-    for (; k < nr; ++k) {
-      const BwRow d = rows[k];
-      if (j >= d.first) csub_mul(w, ldf(vals + d.off + (j - d.first)), X[d.dpos]);
-    }
-  }
-  // x_j = w_j + sum_{i>j} Linv[i][j] w_i
-  const cplx* Linv = vals + sn.diag_off;
-  cplx x = w;
-  const int n = live ? sn.n : 0;
-  for (int i = 1; i < n; ++i) {
-    const cplx wi = cmk(__shfl_sync(0xffffffffu, w.x, i, G), __shfl_sync(0xffffffffu, w.y, i, G));
-    if (col && i > j) cfma(x, ldf(Linv + (long long)i * (i - 1) / 2 + j), wi);
-  }
-  if (col) A.X[(long long)t * A.nw + sn.c0 + j] = x;
-}
-
-// ---------------------------------------------------------- split variants
-// Levels whose per-output loops are long (top of the tree) use more threads per
-// output so no single thread walks a long dependent chain.
-
-// forward diagonal, one WARP per (class, row, member); lanes over j < i
-__global__ void __launch_bounds__(kThreads) k_fwd_diag_warp(SolveArgs A, int ncls,
-                                                            const int2* items, int nitem) {
-  int c, it, t;
-  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (!decode(A, ncls, w, nitem, c, it, t)) return;
-  const int2 item = items[it];
-  const DevSn sn = A.sn[item.x];
-  const int i = item.y;
-  const cplx* row = A.vals + (long long)c * A.nvals + sn.diag_off + (long long)i * (i - 1) / 2;
-  const cplx* y = A.Y + (long long)t * A.nw + sn.c0;
-  cplx acc = cmk(0, 0);
-  for (int j = lane; j < i; j += 32) cfma(acc, ldf(row + j), y[j]);
-  acc = warp_sum(acc);
-  if (lane == 0) A.X[(long long)t * A.nw + sn.c0 + i] = cadd(y[i], acc);
-}
-
-// backward, one CTA per (class, 32-column chunk, member): lanes over columns,
-// the 8 warps split the inner range, partial sums combined in fixed warp order.
-// items: (supernode, first column of the chunk)
-template <bool DIAG>
-__global__ void __launch_bounds__(256) k_bwd_split(SolveArgs A, int ncls, const int2* items,
-                                                   int nitem) {
-  __shared__ cplx part[8][32];
-  int c, it, t;
-  if (!decode(A, ncls, blockIdx.x, nitem, c, it, t)) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int2 item = items[it];
-  const DevSn sn = A.sn[item.x];
-  const int j = item.y + lane;
-  const bool ok = j < sn.n;
-  const cplx* vals = A.vals + (long long)c * A.nvals;
-  cplx acc = cmk(0, 0);
-  if (DIAG) {
-    // x_j = y_j + sum_{i>j} Linv[i][j] y_i ; warps split i
-    const cplx* Linv = vals + sn.diag_off;
-    const cplx* y = A.Y + (long long)t * A.nw + sn.c0;
-    if (ok)
-      for (int i = item.y + 1 + warp; i < sn.n; i += 8)
-        if (i > j) cfma(acc, ldf(Linv + (long long)i * (i - 1) / 2 + j), y[i]);
-  } else {
-    // w_j = Dinv z_j - sum_rows L[r][j] x_r ; warps split the rows
-    const cplx* X = A.X + (long long)t * A.nw;
-    const BwRow* rows = A.bw + A.bw_ptr[item.x];
-    const int nr = A.bw_ptr[item.x + 1] - A.bw_ptr[item.x];
-    if (ok) acc = bw_gather<4>(vals, rows, warp, nr, 8, j, X);
-  }
-  part[warp][lane] = acc;
-  __syncthreads();
-  if (warp == 0 && ok) {
-    cplx sum = part[0][lane];
-    for (int w = 1; w < 8; ++w) sum = cadd(sum, part[w][lane]);
-    const long long p = (long long)t * A.nw + sn.c0 + j;
-    if (DIAG)
-      A.X[p] = cadd(A.Y[p], sum);
-    else
-      A.Y[p] = csub(cmul(ldg(vals + sn.dinv_off + j), A.X[p]), sum);
-  }
-}
-
 // ------------------------------------------------------------------ launcher
-// One class's solve on one stream: the kernels see a single-class view
-// (act_ptr and vals offset to class c), so their class decode is trivial.
-void launch_solve_class(const SolveArgs& A0, const SolvePlan& P, int c, int members,
-                        cudaStream_t st) {
-  SolveArgs A = A0;
-  A.act_ptr = A0.act_ptr + c;
-  A.vals = A0.vals + (long long)c * A0.nvals;
-  launch_solve(A, P, 1, members, st);
-}
-
 int solve_launch_count(const SolvePlan& P) {
-  int n = 2 + 2;
-  for (const auto& L : P.fwd) n += L.small_g ? 1 : 2;
-  for (const auto& L : P.bwd) n += L.small_g ? 1 : 2;
-  return n;
+  return int(P.groups.size()) * (4 + 2 * int(P.fwd.size()) + 2 * int(P.bwd.size()));
 }
 
-static unsigned grid_for(long long work) {
-  return unsigned((work + kThreads - 1) / kThreads);
+static unsigned blocks_for(long long threads) {
+  return unsigned((threads + kThreads - 1) / kThreads);
 }
 
-void launch_solve(const SolveArgs& A, const SolvePlan& P, int ncls, int max_rhs,
-                  cudaStream_t st) {
-  k_ring<<<grid_for((long long)max_rhs * A.nring), kThreads, 0, st>>>(A, ncls);
+static int pow2_floor(long v) {
+  int p = 1;
+  while (2L * p <= v) p <<= 1;
+  return p;
+}
+
+// lanes per output for a forward pull/diagonal level with mean inner length avg
+static int fwd_lanes(int M, long avg) {
+  if (M == 1) return std::max(1, std::min(32, pow2_floor(avg / 4)));
+  if (avg > 128) return std::max(1, pow2_floor(32 / M));
+  return 1;
+}
+
+static TileArg with_shape(TileArg T, int E) {
+  T.E = E;
+  T.R = std::max(1, 32 / (E * T.M));
+  return T;
+}
+
+// Profiling aid for hddm_time_solve (results invalid): HDDM_SKIP is a bit mask of kernel families
+// left out of the solve -- 1 ring, 2 forward leaves, 4 forward pulls, 8 forward
+// diagonals, 16 backward pulls, 32 backward diagonals, 64 leaf columns,
+// 128 backward leaves -- so their marginal cost in the concurrent graph can be
+// timed.
+static int g_skip = 0, g_only = -1;
+static int skip_mask() { return g_skip; }
+void set_solve_skip(int mask, int only_tile) {
+  g_skip = mask;
+  g_only = only_tile;
+}
+
+// staged backward pull over a level's column chunks
+template <bool TO_X>
+static void launch_bwd_stage(const SolveArgs& A, const TileArg& T, const SolveLevel& L,
+                             cudaStream_t st) {
+  constexpr int kBudget = 48 * 1024;
+  const int rowb = (T.M + L.cw_max + 1) * int(sizeof(cplx));
+  const int RC = std::max(1, (kBudget - kStageThreads * int(sizeof(cplx))) / rowb);
+  const size_t smem = size_t(RC) * rowb + kStageThreads * sizeof(cplx);
+  k_bwd_stage<TO_X><<<unsigned((long long)T.ntile * L.nchunk4), kStageThreads, smem, st>>>(
+      A, T, L.d_chunks4, L.nchunk4, RC, L.cw_max);
+}
+
+// one tile group's full solve on one stream
+void launch_solve_group(const SolveArgs& A, const SolvePlan& P, int g, cudaStream_t st) {
+  const int skip = skip_mask();
+  if (g_only >= 0 && g != g_only) return;
+  const TileArg T1 = with_shape(P.groups[g], 1);  // thread per (item, member)
+  const long long nt = T1.ntile;
+  auto blocks = [nt](long long items, int R) { return blocks_for(nt * ((items + R - 1) / R) * 32); };
+  if (!(skip & 1)) k_ring<<<blocks(A.nring, T1.R), kThreads, 0, st>>>(A, T1);
   const SolveLevel& FL = P.fwd_leaf;
-  k_fwd_leaf<<<grid_for((long long)max_rhs * FL.nitem), kThreads, 0, st>>>(A, ncls, FL.d_items,
-                                                                          FL.nitem);
+  if (!(skip & 2))
+    k_fwd_leaf<<<blocks(FL.nitem, T1.R), kThreads, 0, st>>>(A, T1, FL.d_items, FL.nitem);
   for (const auto& L : P.fwd) {
-    if (L.small_g) {
-      const long long w = (long long)max_rhs * L.nsmall * L.small_g;
-      if (L.small_g == 8) k_fwd_small<8><<<grid_for(w), kThreads, 0, st>>>(A, ncls, L.d_small, L.nsmall);
-      else if (L.small_g == 16) k_fwd_small<16><<<grid_for(w), kThreads, 0, st>>>(A, ncls, L.d_small, L.nsmall);
-      else k_fwd_small<32><<<grid_for(w), kThreads, 0, st>>>(A, ncls, L.d_small, L.nsmall);
-      continue;
+    // one item per CTA (8 warps share the inner loop) when items are long
+    const unsigned gc = unsigned(nt * L.nitem);
+    const TileArg Tw = with_shape(T1, std::max(1, 32 / T1.M));  // widest lanes, R = 1
+    if (skip & 4) {
+    } else if (L.avg_run > P.cta_run) {
+      k_fwd_cta<false><<<gc, kThreads, 0, st>>>(A, Tw, L.d_rec, L.d_items, L.nitem);
+    } else {
+      const TileArg Tp = with_shape(T1, fwd_lanes(T1.M, L.avg_run));
+      k_fwd_pull<<<blocks(L.nitem, Tp.R), kThreads, 0, st>>>(A, Tp, L.d_rec, L.nitem);
     }
-    const unsigned g = grid_for((long long)max_rhs * L.nitem);
-    const unsigned gw = grid_for((long long)max_rhs * L.nitem * 32);
-    const long long w = (long long)max_rhs * L.nitem;
-    switch (L.group) {
-      case 32: k_fwd_pull_warp<<<gw, kThreads, 0, st>>>(A, ncls, L.d_rec, L.nitem); break;
-      case 16: k_fwd_pull_sub<16><<<grid_for(w * 16), kThreads, 0, st>>>(A, ncls, L.d_items, L.nitem); break;
-      case 8: k_fwd_pull_sub<8><<<grid_for(w * 8), kThreads, 0, st>>>(A, ncls, L.d_items, L.nitem); break;
-      case 4: k_fwd_pull_sub<4><<<grid_for(w * 4), kThreads, 0, st>>>(A, ncls, L.d_items, L.nitem); break;
-      default: k_fwd_pull<<<g, kThreads, 0, st>>>(A, ncls, L.d_rec, L.nitem); break;
+    if (skip & 8) {
+    } else if (L.avg_diag > P.cta_diag) {
+      k_fwd_cta<true><<<gc, kThreads, 0, st>>>(A, Tw, L.d_rec, L.d_items, L.nitem);
+    } else {
+      const TileArg Td = with_shape(T1, fwd_lanes(T1.M, L.avg_diag));
+      k_fwd_diag<<<blocks(L.nitem, Td.R), kThreads, 0, st>>>(A, Td, L.d_items, L.nitem);
     }
-    if (L.warp_diag)
-      k_fwd_diag_warp<<<gw, kThreads, 0, st>>>(A, ncls, L.d_items, L.nitem);
-    else
-      k_fwd_diag<<<g, kThreads, 0, st>>>(A, ncls, L.d_items, L.nitem);
   }
   for (const auto& L : P.bwd) {
-    if (L.small_g) {
-      const long long w = (long long)max_rhs * L.nsmall * L.small_g;
-      if (L.small_g == 8) k_bwd_small<8><<<grid_for(w), kThreads, 0, st>>>(A, ncls, L.d_small, L.nsmall);
-      else if (L.small_g == 16) k_bwd_small<16><<<grid_for(w), kThreads, 0, st>>>(A, ncls, L.d_small, L.nsmall);
-      else k_bwd_small<32><<<grid_for(w), kThreads, 0, st>>>(A, ncls, L.d_small, L.nsmall);
-      continue;
-    }
-    const unsigned g = grid_for((long long)max_rhs * L.nitem);
-    if (L.nchunk > 0) {
-      const unsigned gc = unsigned((long long)max_rhs * L.nchunk);
-      if (L.warp_rows)
-        k_bwd_split<false><<<gc, 256, 0, st>>>(A, ncls, L.d_chunks, L.nchunk);
-      else
-        k_bwd_pull<false><<<g, kThreads, 0, st>>>(A, ncls, L.d_items, L.nitem);
-      if (L.warp_diag)
-        k_bwd_split<true><<<gc, 256, 0, st>>>(A, ncls, L.d_chunks, L.nchunk);
-      else
-        k_bwd_diag<<<g, kThreads, 0, st>>>(A, ncls, L.d_items, L.nitem);
-    } else {
-      k_bwd_pull<false><<<g, kThreads, 0, st>>>(A, ncls, L.d_items, L.nitem);
-      k_bwd_diag<<<g, kThreads, 0, st>>>(A, ncls, L.d_items, L.nitem);
-    }
+    // split kernels: one CTA per (tile, group of R = 32 / M consecutive columns)
+    const auto grp = L.groups.find(T1.R);
+    const bool has_grp = grp != L.groups.end();
+    const unsigned gs = has_grp ? unsigned(nt * grp->second.first) : 0;
+    if (skip & 16) {
+    } else if (P.staged)
+      launch_bwd_stage<false>(A, T1, L, st);
+    else if (L.split_rows && has_grp)
+      k_bwd_split<false><<<gs, kThreads, 0, st>>>(A, T1, grp->second.second, grp->second.first);
+    else
+      k_bwd_pull<false><<<blocks(L.nitem, T1.R), kThreads, 0, st>>>(A, T1, L.d_items, L.nitem);
+    if (skip & 32) {
+    } else if (L.split_diag && has_grp)
+      k_bwd_split<true><<<gs, kThreads, 0, st>>>(A, T1, grp->second.second, grp->second.first);
+    else
+      k_bwd_diag<<<blocks(L.nitem, T1.R), kThreads, 0, st>>>(A, T1, L.d_items, L.nitem);
   }
   const SolveLevel& BC = P.bwd_leafcol;
-  k_bwd_pull<true><<<grid_for((long long)max_rhs * BC.nitem), kThreads, 0, st>>>(
-      A, ncls, BC.d_items, BC.nitem);
+  if (!(skip & 64)) {
+    if (P.staged)
+      launch_bwd_stage<true>(A, T1, BC, st);
+    else
+      k_bwd_pull<true><<<blocks(BC.nitem, T1.R), kThreads, 0, st>>>(A, T1, BC.d_items, BC.nitem);
+  }
   const SolveLevel& BL = P.bwd_leaf;
-  k_bwd_leaf<<<grid_for((long long)max_rhs * BL.nitem), kThreads, 0, st>>>(A, ncls, BL.d_items,
-                                                                          BL.nitem);
+  if (!(skip & 128))
+    k_bwd_leaf<<<blocks(BL.nitem, T1.R), kThreads, 0, st>>>(A, T1, BL.d_items, BL.nitem);
 }
 
 }  // namespace hddm

@@ -22,7 +22,7 @@ import numpy as np
 from .problems import Problem
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhddm.so")
+LIB_PATH = os.environ.get("HDDM_LIB") or os.path.join(HERE, "libhddm.so")
 
 HDDM_HOST, HDDM_DEVICE = 0, 1
 
