@@ -133,6 +133,16 @@ def barrier(world: int):
         dist.barrier()
 
 
+def solve_traffic():
+    """Solve-stage DRAM bytes per solve from the committed ncu step summary."""
+    path = os.path.join(ROOT, "profiles", "r01_step_summary.json")
+    try:
+        with open(path) as f:
+            return json.load(f)["solve_dram_bytes"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def dense_residual(prob, seed: int = 1234) -> np.ndarray:
     """Seeded dense complex vector, zero on the global ring (an FGMRES Krylov
     vector after the first iteration is dense)."""
@@ -282,7 +292,11 @@ def run_ours(args, world, rank, local):
                        "step": "one DDM sweep of precondition(r, K=steps), dense r"},
             "munknown_iters_per_s": value * prob.n_global / 1e6,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "frac": (achieved / peak) if achieved else None,
+                         "traffic": solve_traffic(),
+                         "traffic_note": "DRAM bytes of the solve-stage kernels of one step, "
+                                         "profiles/r01_step_summary.json (ncu, cache flushed "
+                                         "per launch: an upper bound)",
                          "kernel": "batched supernodal solve stage (fwd+bwd, all classes)",
                          "bytes_per_launch": B["B_solve"], "ms_per_launch": solve_ms_per,
                          "peak_kind": peak_kind},

@@ -638,8 +638,6 @@ void hddm_engine::build_plan() {
     L.cw_max = cw;
   };
   plan.staged = std::getenv("HDDM_NO_STAGE") == nullptr;
-  if (const char* v = std::getenv("HDDM_CTA_RUN")) plan.cta_run = std::atol(v);
-  if (const char* v = std::getenv("HDDM_CTA_DIAG")) plan.cta_diag = std::atol(v);
   plan.fwd_leaf = level(leaves);
   plan.bwd_leaf = level(leaves);
   plan.bwd_leafcol = level(leafcols);

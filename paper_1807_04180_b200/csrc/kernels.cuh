@@ -79,8 +79,6 @@ struct SolvePlan {
   bool staged = true;                  // backward pulls through shared memory
   // forward: CTA per row above these mean lengths (measured slower at config 4:
   // off by default, HDDM_CTA_RUN / HDDM_CTA_DIAG)
-  long cta_run = 1L << 40;
-  long cta_diag = 1L << 40;
 };
 
 // one tile group's full solve (all levels) on one stream

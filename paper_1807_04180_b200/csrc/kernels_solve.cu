@@ -251,64 +251,6 @@ __global__ void __launch_bounds__(kThreads) k_fwd_pull(SolveArgs A, TileArg T, c
   }
 }
 
-// Long runs (top levels): a CTA of 8 warps per (tile, row); warp w strides the
-// run with its E element lanes at offset w * E, partial sums combined in fixed
-// warp order. DIAG: the dense-inverse row instead of the incoming run.
-template <bool DIAG>
-__global__ void __launch_bounds__(kThreads) k_fwd_cta(SolveArgs A, TileArg T, const int4* rec,
-                                                      const int2* items, int nitem) {
-  __shared__ cplx part[8][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int ti = blockIdx.x / nitem;
-  const int it = blockIdx.x - ti * nitem;
-  TL L;
-  L.k = lane % T.M;
-  L.e = (lane / T.M) % T.E;
-  L.r = lane / (T.M * T.E);
-  L.it = it;
-  tile_fill(A, T, ti, L.r == 0, L);
-  cplx acc = cmk(0, 0);
-  long long out = 0;
-  if (L.act) {
-    if (DIAG) {
-      const int2 item = items[it];
-      const DevSn sn = A.sn[item.x];
-      const int i = item.y;
-      const SVec<const cplx> y{A.Y + vat(L, sn.c0), L.m};
-      const cplx* row = A.vals + (long long)L.c * A.nvals + sn.diag_off + (long long)i * (i - 1) / 2;
-      cplx a2 = cmk(0, 0);
-      const int st = 8 * T.E;
-      int j = warp * T.E + L.e;
-      for (; j + st < i; j += 2 * st) {
-        const cplx l0 = ldf(row + j), l1 = ldf(row + j + st);
-        const cplx v0 = y[j], v1 = y[j + st];
-        cfma(acc, l0, v0);
-        cfma(a2, l1, v1);
-      }
-      if (j < i) cfma(acc, ldf(row + j), y[j]);
-      acc = cadd(acc, a2);
-      out = vat(L, sn.c0 + i);
-    } else {
-      const int4 R = __ldg(rec + it);
-      const long long r0 = (long long)(unsigned)R.z | ((long long)R.w << 32);
-      acc = gather_dot<kUF>(A.vals + (long long)L.c * A.nvals + r0, A.zidx + r0,
-                            warp * T.E + L.e, R.y, 8 * T.E, A.X + L.cb, L.m);
-      out = vat(L, R.x);
-    }
-  }
-  if (T.E > 1) acc = tile_reduce(acc, T, L);
-  part[warp][lane] = acc;
-  __syncthreads();
-  if (warp == 0 && L.act && L.e == 0) {
-    cplx sum = part[0][lane];
-    for (int w = 1; w < 8; ++w) sum = cadd(sum, part[w][lane]);
-    if (DIAG)
-      A.X[out] = cadd(A.Y[out], sum);
-    else
-      A.Y[out] = csub(A.B[out], sum);
-  }
-}
-
 // separator rows, forward diagonal: X[i] = Y[i] + sum_{j<i} Linv[i][j] Y[j]
 __global__ void __launch_bounds__(kThreads) k_fwd_diag(SolveArgs A, TileArg T, const int2* items,
                                                        int nitem) {
@@ -640,20 +582,11 @@ void launch_solve_group(const SolveArgs& A, const SolvePlan& P, int g, cudaStrea
   if (!(skip & 2))
     k_fwd_leaf<<<blocks(FL.nitem, T1.R), kThreads, 0, st>>>(A, T1, FL.d_items, FL.nitem);
   for (const auto& L : P.fwd) {
-    // one item per CTA (8 warps share the inner loop) when items are long
-    const unsigned gc = unsigned(nt * L.nitem);
-    const TileArg Tw = with_shape(T1, std::max(1, 32 / T1.M));  // widest lanes, R = 1
-    if (skip & 4) {
-    } else if (L.avg_run > P.cta_run) {
-      k_fwd_cta<false><<<gc, kThreads, 0, st>>>(A, Tw, L.d_rec, L.d_items, L.nitem);
-    } else {
+    if (!(skip & 4)) {
       const TileArg Tp = with_shape(T1, fwd_lanes(T1.M, L.avg_run));
       k_fwd_pull<<<blocks(L.nitem, Tp.R), kThreads, 0, st>>>(A, Tp, L.d_rec, L.nitem);
     }
-    if (skip & 8) {
-    } else if (L.avg_diag > P.cta_diag) {
-      k_fwd_cta<true><<<gc, kThreads, 0, st>>>(A, Tw, L.d_rec, L.d_items, L.nitem);
-    } else {
+    if (!(skip & 8)) {
       const TileArg Td = with_shape(T1, fwd_lanes(T1.M, L.avg_diag));
       k_fwd_diag<<<blocks(L.nitem, Td.R), kThreads, 0, st>>>(A, Td, L.d_items, L.nitem);
     }
