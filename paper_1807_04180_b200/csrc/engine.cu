@@ -118,7 +118,7 @@ struct hddm_engine {
   int* d_act_list = nullptr;
   long long* d_counts = nullptr;
   double* d_part_chk = nullptr;
-  int nchunk = 8;
+  int nchunk = 64;  // residual-check partials per subdomain (position chunks)
   double* d_rel = nullptr;
   int* d_refine = nullptr;
   double* d_maxrel = nullptr;
@@ -317,6 +317,8 @@ void hddm_engine::create(const hddm_problem& p) {
   ng = (long long)S.gnx * S.gny;
   for (int c = 0; c < ncls; ++c)
     max_members = std::max(max_members, S.cls_ptr[c + 1] - S.cls_ptr[c]);
+  if (max_members > 256)  // the residual check assigns one member per thread
+    throw ConfigErr("a factor class with more than 256 subdomains is not supported");
   build_symbolic(wnx, wny, Y);
 
   // ---- symbolic tables
@@ -993,9 +995,10 @@ void hddm_engine::enqueue_step_front(int s, cudaStream_t stream, unsigned long l
   const StepArgs A = step_args(s, d_f);
   launch_flags(A, ncls, stream);
   launch_gather(A, stream);
-  enqueue_solve(solve_args(d_B, A.Ucur, d_Y, A.zc, 0), stream);
+  static const bool no_solve = std::getenv("HDDM_STEP_NOSOLVE") != nullptr;  // profiling aid
+  if (!no_solve) enqueue_solve(solve_args(d_B, A.Ucur, d_Y, A.zc, 0), stream);
   launch_check(check_args(d_B, A.Ucur, A.zc, nullptr), stream);
-  launch_refine_init(refine_args(d_B, A.Ucur, A.zc, cond), stream);
+  if (!no_solve) launch_refine_init(refine_args(d_B, A.Ucur, A.zc, cond), stream);
 }
 
 // The batched solve on `stream`. On the engine stream, every class runs its

@@ -231,7 +231,12 @@ __global__ void __launch_bounds__(256) k_rhs_transfer(StepArgs A) {
 }
 
 void launch_gather(const StepArgs& A, cudaStream_t st) {
-  k_rhs_base<<<unsigned((A.vm.total + 255) / 256), 256, 0, st>>>(A);
+  // steps >= 2 see no f: every base value is 0. Right-hand sides of inactive
+  // subdomains are never read, so all of B is cleared at memset speed.
+  if (A.step == 1)
+    k_rhs_base<<<unsigned((A.vm.total + 255) / 256), 256, 0, st>>>(A);
+  else
+    cudaMemsetAsync(A.B, 0, size_t(A.vm.total) * sizeof(cplx), st);
   dim3 g2((A.npatch + 255) / 256, A.nsub);
   k_rhs_transfer<<<g2, 256, 0, st>>>(A);
 }
@@ -299,34 +304,49 @@ __device__ __forceinline__ cplx ax_row(XV X, int pos, int wnx, int wny,
   return ax;
 }
 
+// Residual partials in storage order: block (chunk, class c); thread t serves
+// member k = t % m at positions t / m, t / m + 256 / m, ... of the chunk, so a
+// warp reads consecutive members (contiguous addresses). Members of a class have
+// bitwise-identical window operators (the class criterion), so the stencil
+// coefficients come from the class representative. Per-member sums combine in
+// fixed thread order.
 __global__ void __launch_bounds__(256) k_check(CheckArgs A) {
-  __shared__ double sh[32];
-  const int t = blockIdx.y;
-  const bool act = A.only ? A.only[t] != 0 : !A.zc[t];
+  __shared__ double sr[256], sb[256];
+  const int c = blockIdx.y;
+  const int c0 = A.vm.cptr[c], m = A.vm.cptr[c + 1] - c0;
+  const int tid = threadIdx.x;
+  const int per = 256 / m;  // positions per sweep of the block (m <= 256)
+  const int k = tid % m, pi = tid / m;
+  const int t = A.vm.cmem[c0 + k];
+  const bool act = pi < per && (A.only ? A.only[t] != 0 : !A.zc[t]);
   double r2 = 0, b2 = 0;
   if (act) {
-    const SVec<const cplx> X = vview(A.X, A.vm, t);
-    const SVec<const cplx> Bv = vview(A.B, A.vm, t);
-    const DevSub T = A.sub[t];
-    const cplx* sa = A.sa + (long long)t * A.sa_stride;
-    const cplx* a1n = sa;
-    const cplx* ia1h = sa + A.wnx;
-    const cplx* a2n = sa + 2 * A.wnx;
-    const cplx* ia2h = sa + 2 * A.wnx + A.wny;
+    const int rep = A.vm.cmem[c0];
+    const DevSub T = A.sub[rep];
+    const cplx* sa = A.sa + (long long)rep * A.sa_stride;
+    const SVec<const cplx> X{A.X + A.vm.cbase[c] + k, m};
+    const SVec<const cplx> Bv{A.B + A.vm.cbase[c] + k, m};
     const int chunk = (A.nw + A.nchunk - 1) / A.nchunk;
     const int p0 = blockIdx.x * chunk, p1 = min(A.nw, p0 + chunk);
-    for (int pos = p0 + threadIdx.x; pos < p1; pos += blockDim.x) {
+    for (int pos = p0 + pi; pos < p1; pos += per) {
       const cplx b = Bv[pos];
       b2 += cnorm2(b);
       const cplx ax = ax_row(X, pos, A.wnx, A.wny, A.gnx, A.ih2, T, sa, A.k2, A.perm, A.pinv);
       r2 += cnorm2(csub(b, ax));
     }
   }
-  const double R = block_sum(r2, sh);
-  const double Bs = block_sum(b2, sh);
-  if (threadIdx.x == 0) {
-    A.part[((long long)t * A.nchunk + blockIdx.x) * 2 + 0] = R;
-    A.part[((long long)t * A.nchunk + blockIdx.x) * 2 + 1] = Bs;
+  sr[tid] = r2;
+  sb[tid] = b2;
+  __syncthreads();
+  if (tid < m) {
+    double R = 0, Bs = 0;
+    for (int q = tid; q < per * m; q += m) {
+      R += sr[q];
+      Bs += sb[q];
+    }
+    const int tk = A.vm.cmem[c0 + tid];
+    A.part[((long long)tk * A.nchunk + blockIdx.x) * 2 + 0] = R;
+    A.part[((long long)tk * A.nchunk + blockIdx.x) * 2 + 1] = Bs;
   }
 }
 
@@ -348,12 +368,12 @@ __global__ void k_check_finish(CheckArgs A, int nsub) {
 }
 
 void launch_check_partials(const CheckArgs& A, cudaStream_t st) {
-  dim3 g(A.nchunk, A.nsub);
+  dim3 g(A.nchunk, A.vm.ncls);
   k_check<<<g, 256, 0, st>>>(A);
 }
 
 void launch_check(const CheckArgs& A, cudaStream_t st) {
-  dim3 g(A.nchunk, A.nsub);
+  dim3 g(A.nchunk, A.vm.ncls);
   k_check<<<g, 256, 0, st>>>(A);
   k_check_finish<<<1, 256, 0, st>>>(A, A.nsub);
 }
