@@ -11,6 +11,8 @@
 //   DdmEngine::precondition           ddm.hpp:78
 //   DdmEngine::class_info             ddm.hpp:63
 //   fgmres                            proj/include/helmddm/krylov.hpp:31-33
+//   run_cli, parse_config_text,       proj/include/helmddm/cli.hpp,
+//   make_setup, the artifact writers  config.hpp, io.hpp (CLI parity)
 // and the error -> exit-code mapping of proj/src/cli.cpp:453-469.
 #include <chrono>
 #include <complex>
@@ -20,7 +22,10 @@
 #include <stdexcept>
 #include <vector>
 
+#include "helmddm/cli.hpp"
+#include "helmddm/config.hpp"
 #include "helmddm/ddm.hpp"
+#include "helmddm/io.hpp"
 #include "helmddm/krylov.hpp"
 #include "helmddm/oracle.hpp"
 
@@ -254,6 +259,94 @@ int ref_direct_solve(const ref_problem* p, const double* f, double* out) {
     const FieldGrid u =
         direct_solve_global(cfg.grid, cfg.medium, cfg.c_sigma, fv, cfg.sigma0);
     std::memcpy(out, u.v.data(), n * sizeof(Complex));
+    return 0;
+  } catch (...) {
+    return map_error();
+  }
+}
+
+// ---------------------------------------------------------------- CLI parity
+// The reference command line in-process (proj/src/cli.cpp:453).
+int ref_run_cli(int argc, char** argv) { return run_cli(argc, argv); }
+
+struct ref_setup_out {
+  int mx, my, n1, n2, n_overlap, n_ramp;
+  double h, x0, y0, omega;
+  int medium_kind;  // 0 constant, 1 layered
+  double velocity;
+  int n_layers;
+  double layer_ylo[64], layer_yhi[64], layer_c[64];
+  int source_kind;  // 0 gaussian, 1 point
+  double source_x, source_y, k_source;
+  double c_sigma, sigma0;
+  int mode;         // 0 ddm, 1 fgmres, 2 direct
+  double tol, krylov_tol;
+  int max_steps, check_every, precond_k, krylov_max_iter, krylov_restart, threads;
+};
+
+// parse_config_text + make_setup (config.cpp:155-228); overrides are
+// newline-separated key=value pairs. Returns the CLI exit code of a failure.
+int ref_setup(const char* text, const char* overrides, ref_setup_out* o, char* err, int errlen) {
+  try {
+    std::vector<std::string> ov;
+    std::string all = overrides ? overrides : "";
+    size_t a = 0;
+    while (a < all.size()) {
+      size_t b = all.find('\n', a);
+      if (b == std::string::npos) b = all.size();
+      if (b > a) ov.push_back(all.substr(a, b - a));
+      a = b + 1;
+    }
+    const RunConfig c = parse_config_text(text, ov);
+    const ProblemSetup st = make_setup(c);
+    o->mx = st.grid.mx;
+    o->my = st.grid.my;
+    o->n1 = st.grid.n1;
+    o->n2 = st.grid.n2;
+    o->n_overlap = st.grid.n_overlap;
+    o->n_ramp = st.grid.n_ramp;
+    o->h = st.grid.h;
+    o->x0 = st.grid.x0;
+    o->y0 = st.grid.y0;
+    o->omega = st.medium.omega;
+    o->medium_kind = st.medium.kind == MediumKind::Constant ? 0 : 1;
+    o->velocity = st.medium.velocity;
+    o->n_layers = int(std::min<size_t>(64, st.medium.layers.size()));
+    for (int i = 0; i < o->n_layers; ++i) {
+      o->layer_ylo[i] = st.medium.layers[i].y_lo;
+      o->layer_yhi[i] = st.medium.layers[i].y_hi;
+      o->layer_c[i] = st.medium.layers[i].velocity;
+    }
+    o->source_kind = st.source.kind == SourceKind::PointDelta ? 1 : 0;
+    o->source_x = st.source.x;
+    o->source_y = st.source.y;
+    o->k_source = st.k_source;
+    o->c_sigma = c.c_sigma;
+    o->sigma0 = c.sigma0;
+    o->mode = c.mode == "ddm" ? 0 : c.mode == "fgmres" ? 1 : 2;
+    o->tol = c.tol;
+    o->krylov_tol = c.krylov_tol;
+    o->max_steps = c.max_steps;
+    o->check_every = c.check_every;
+    o->precond_k = c.precond_k;
+    o->krylov_max_iter = c.krylov_max_iter;
+    o->krylov_restart = c.krylov_restart;
+    o->threads = c.threads;
+    return 0;
+  } catch (const std::exception& e) {
+    if (err && errlen > 0) std::snprintf(err, size_t(errlen), "%s", e.what());
+    return map_error();
+  }
+}
+
+// sample_source on the global window of the setup above (medium.cpp:52-73).
+int ref_sample_source(const char* text, double* out) {
+  try {
+    const RunConfig c = parse_config_text(text, {});
+    const ProblemSetup st = make_setup(c);
+    const FieldGrid f =
+        sample_source(st.source, st.grid.lattice(), st.grid.global_window(), st.k_source);
+    std::memcpy(out, f.v.data(), f.v.size() * sizeof(Complex));
     return 0;
   } catch (...) {
     return map_error();
