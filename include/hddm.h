@@ -144,6 +144,12 @@ int hddm_class_solve(hddm_engine* e, int c, const double* b, double* x,
 /* Window node counts and the reference elimination order (perm[pos] = node). */
 int hddm_window_dims(const hddm_engine* e, int* nx, int* ny);
 int hddm_nd_order(int nx, int ny, int* order);
+/* Factor entries one class's forward sweep reads: the full sweep (= nnz(L)) and
+ * the sweep of steps >= 2, whose right-hand sides are nonzero only on the
+ * transfer patches (subtrees without patch nodes are skipped; SURVEY 8(d) counts
+ * only the blocks read). Measurement accessor. */
+int hddm_fwd_entries(const hddm_engine* e, long long* full, long long* sparse_rhs);
+
 /* Host-only symbolic analysis of an nx-by-ny window (no GPU needed):
  * the reference's factor_nonzeros() (nnz(L)+n, sparse.cpp:238-240), the
  * strictly-lower entries the engine stores, supernode count, tree height. */

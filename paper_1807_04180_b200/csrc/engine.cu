@@ -215,6 +215,7 @@ struct hddm_engine {
   SolveArgs solve_args(const cplx* B, cplx* X, cplx* Y, const int* flag, int on);
   void enqueue_solve(const SolveArgs& A, cudaStream_t stream);
   int* d_zero = nullptr;  // nsub zero flags: every RHS active
+  long long fwd_entries_full = 0, fwd_entries_sparse = 0;  // factor entries per forward sweep
   VMap vmap() const {
     VMap m;
     m.base = d_vbase;
@@ -287,6 +288,25 @@ struct hddm_engine {
   long long stage_n[kStages] = {};
   void ensure_krylov(int m);
   void build_plan();
+  // window nodes in the union of the 8 transfer patches (transfer.cpp:7-62;
+  // identical for every window): the only nonzero RHS entries after step 1
+  std::vector<int> patch_union_mask() const {
+    const int ext = S.ext, nov = S.nov;
+    const int cx0 = ext, cx1 = ext + S.mcx, cy0 = ext, cy1 = ext + S.mcy;
+    std::vector<int> mask(size_t(wnx) * wny, 0);
+    for (int d = 0; d < 8; ++d) {
+      int p0 = 1, p1 = wnx - 2, q0 = 1, q1 = wny - 2;
+      const bool fL = d == 1 || d == 5 || d == 7, fR = d == 0 || d == 4 || d == 6;
+      const bool fB = d == 3 || d == 6 || d == 7, fT = d == 2 || d == 4 || d == 5;
+      if (fL) { p0 = std::max(p0, cx0 + 1); p1 = std::min(p1, cx0 + 1 + nov); }
+      if (fR) { p0 = std::max(p0, cx1 - 1 - nov); p1 = std::min(p1, cx1 - 1); }
+      if (fB) { q0 = std::max(q0, cy0 + 1); q1 = std::min(q1, cy0 + 1 + nov); }
+      if (fT) { q0 = std::max(q0, cy1 - 1 - nov); q1 = std::min(q1, cy1 - 1); }
+      for (int q = q0; q <= q1; ++q)
+        for (int pp = p0; pp <= p1; ++pp) mask[size_t(q) * wnx + pp] |= 1 << d;
+    }
+    return mask;
+  }
   int solve_launches() const { return solve_launch_count(plan); }
 };
 
@@ -529,22 +549,7 @@ void hddm_engine::create(const hddm_problem& p) {
   // union of the transfer patches in window-local coordinates
   // (transfer_patch, transfer.cpp:7-62; identical for every window)
   {
-    const Sub& s0 = S.subs[0];
-    const int ext = S.ext, nov = S.nov;
-    const int cx0 = ext, cx1 = ext + S.mcx, cy0 = ext, cy1 = ext + S.mcy;
-    std::vector<int> mask(size_t(wnx) * wny, 0);
-    for (int d = 0; d < 8; ++d) {
-      int p0 = 1, p1 = wnx - 2, q0 = 1, q1 = wny - 2;
-      const bool fL = d == 1 || d == 5 || d == 7, fR = d == 0 || d == 4 || d == 6;
-      const bool fB = d == 3 || d == 6 || d == 7, fT = d == 2 || d == 4 || d == 5;
-      if (fL) { p0 = std::max(p0, cx0 + 1); p1 = std::min(p1, cx0 + 1 + nov); }
-      if (fR) { p0 = std::max(p0, cx1 - 1 - nov); p1 = std::min(p1, cx1 - 1); }
-      if (fB) { q0 = std::max(q0, cy0 + 1); q1 = std::min(q1, cy0 + 1 + nov); }
-      if (fT) { q0 = std::max(q0, cy1 - 1 - nov); q1 = std::min(q1, cy1 - 1); }
-      for (int q = q0; q <= q1; ++q)
-        for (int pp = p0; pp <= p1; ++pp) mask[size_t(q) * wnx + pp] |= 1 << d;
-    }
-    (void)s0;
+    const std::vector<int> mask = patch_union_mask();
     std::vector<int> pn, pm;
     for (int k = 0; k < nw; ++k) {  // factor order: coalesced writes of B
       const int node = Y.perm[k];
@@ -640,6 +645,7 @@ void hddm_engine::build_plan() {
     L.cw_max = cw;
   };
   plan.staged = std::getenv("HDDM_NO_STAGE") == nullptr;
+  set_solve_pdl(std::getenv("HDDM_PDL") != nullptr);  // measured slower at config 4: opt-in
   plan.fwd_leaf = level(leaves);
   plan.bwd_leaf = level(leaves);
   plan.bwd_leafcol = level(leafcols);
@@ -668,6 +674,64 @@ void hddm_engine::build_plan() {
     L.avg_run = tot / long(v.size());
     L.avg_diag = dtot / long(v.size());
     plan.fwd.push_back(L);
+  }
+  // forward plan for steps >= 2: only the nonzero RHS entries are the transfer
+  // patches, so supernodes whose subtree holds no patch node produce z = 0
+  // exactly (X is cleared first) and are skipped
+  if (std::getenv("HDDM_NO_SPARSE_RHS") == nullptr) {
+    const std::vector<int> mask = patch_union_mask();
+    std::vector<char> act(nsn, 0);
+    for (int s = 0; s < nsn; ++s) {  // postorder: children before parents
+      const SnNode& a = Y.sn[s];
+      char any = 0;
+      for (int i = 0; i < a.n && !any; ++i) any = mask[Y.perm[a.c0 + i]] != 0;
+      for (int c = 0; c < a.nch; ++c) any |= act[a.child[c]];
+      act[s] = any;
+    }
+    std::vector<int2> lv;
+    for (const int2& l : leaves)
+      if (act[l.x]) lv.push_back(l);
+    plan.fwd_leaf_sp = level(lv);
+    for (const SolveLevel& L : plan.fwd) {
+      // the level's rows, filtered to active separators (same order)
+      std::vector<int2> v(L.nitem);
+      CK(cudaMemcpy(v.data(), L.d_items, sizeof(int2) * L.nitem, cudaMemcpyDeviceToHost));
+      std::vector<int2> keep;
+      for (const int2& it : v)
+        if (act[it.x]) keep.push_back(it);
+      SolveLevel F;
+      if (!keep.empty()) {
+        F = level(keep);
+        std::vector<int4> rec(keep.size());
+        long tot = 0, dtot = 0;
+        for (size_t k = 0; k < keep.size(); ++k) {
+          const int pos = Y.sn[keep[k].x].c0 + keep[k].y;
+          const long long ro = Y.run_off[pos];
+          rec[k] = make_int4(pos, int(Y.run_off[pos + 1] - ro), int(ro & 0xffffffffLL), int(ro >> 32));
+          tot += rec[k].y;
+          dtot += keep[k].y;
+        }
+        F.d_rec = upload(rec);
+        F.avg_run = tot / long(keep.size());
+        F.avg_diag = dtot / long(keep.size());
+      }
+      plan.fwd_sp.push_back(F);
+    }
+    plan.has_sparse = true;
+    fwd_entries_full = 0;
+    fwd_entries_sparse = 0;
+    for (int s = 0; s < nsn; ++s) {
+      const SnNode& a = Y.sn[s];
+      long long w = 0;
+      if (a.kind == 1) {
+        for (int i = 0; i < a.n; ++i) w += Y.run_off[a.c0 + i + 1] - Y.run_off[a.c0 + i];
+        w += (long long)a.n * (a.n - 1) / 2;
+      } else {
+        for (int i = 0; i < a.n; ++i) w += i - Y.row_first[a.drow0 + i];
+      }
+      fwd_entries_full += w;
+      if (act[s]) fwd_entries_sparse += w;
+    }
   }
   const char* env_sr = std::getenv("HDDM_SPLIT_ROWS");
   const char* env_sd = std::getenv("HDDM_SPLIT_DIAG");
@@ -805,6 +869,7 @@ SolveArgs hddm_engine::solve_args(const cplx* Bp, cplx* X, cplx* Yp, const int* 
   A.nvals = Y.nvals;
   A.flag = flag;
   A.flag_on = on;
+  A.sparse_rhs = 0;
   A.B = Bp;
   A.X = X;
   A.Y = Yp;
@@ -996,7 +1061,12 @@ void hddm_engine::enqueue_step_front(int s, cudaStream_t stream, unsigned long l
   launch_flags(A, ncls, stream);
   launch_gather(A, stream);
   static const bool no_solve = std::getenv("HDDM_STEP_NOSOLVE") != nullptr;  // profiling aid
-  if (!no_solve) enqueue_solve(solve_args(d_B, A.Ucur, d_Y, A.zc, 0), stream);
+  SolveArgs SA = solve_args(d_B, A.Ucur, d_Y, A.zc, 0);
+  if (s >= 2 && plan.has_sparse) {  // RHS nonzero only on the transfer patches
+    CK(cudaMemsetAsync(A.Ucur, 0, size_t(nsub) * nw * sizeof(cplx), stream));
+    SA.sparse_rhs = 1;
+  }
+  if (!no_solve) enqueue_solve(SA, stream);
   launch_check(check_args(d_B, A.Ucur, A.zc, nullptr), stream);
   if (!no_solve) launch_refine_init(refine_args(d_B, A.Ucur, A.zc, cond), stream);
 }
@@ -1598,6 +1668,13 @@ int hddm_stage_times(hddm_engine* e, double* ms, long long* count, int cap, int*
 }
 
 long long hddm_launch_count(const hddm_engine* e) { return e->launches; }
+
+int hddm_fwd_entries(const hddm_engine* e, long long* full, long long* sparse_rhs) {
+  if (!e || !full || !sparse_rhs) return 1;
+  *full = e->fwd_entries_full ? e->fwd_entries_full : e->Y.nnz_stored;
+  *sparse_rhs = e->plan.has_sparse ? e->fwd_entries_sparse : *full;
+  return 0;
+}
 
 int hddm_time_solve(hddm_engine* e, int reps, double* ms_per_solve) {
   return guarded(e, [&] {

@@ -25,6 +25,7 @@ struct SolveArgs {
   long long nvals;
   const int* flag;     // per RHS t: active iff (flag[t] != 0) == flag_on
   int flag_on;
+  int sparse_rhs;      // host: RHS nonzero only on the transfer patches (forward plan fwd_sp)
   const cplx* B;       // right-hand sides (factor order), layout vm
   cplx* X;             // solutions (factor order), layout vm
   cplx* Y;             // scratch, layout vm
@@ -70,6 +71,9 @@ struct SolveLevel {
 struct SolvePlan {
   SolveLevel fwd_leaf;                 // leaves: band forward substitution
   std::vector<SolveLevel> fwd;         // separator rows by height (pull, then diag)
+  SolveLevel fwd_leaf_sp;              // the same restricted to subtrees holding transfer-
+  std::vector<SolveLevel> fwd_sp;      // patch nodes (steps >= 2; X cleared beforehand)
+  bool has_sparse = false;
   std::vector<SolveLevel> bwd;         // separator columns by depth (pull, then diag)
   SolveLevel bwd_leafcol;              // leaf columns: w = Dinv z - B^T x
   SolveLevel bwd_leaf;                 // leaves: band back-substitution
@@ -85,6 +89,7 @@ struct SolvePlan {
 void launch_solve_group(const SolveArgs& A, const SolvePlan& P, int g, cudaStream_t st);
 int solve_launch_count(const SolvePlan& P);  // kernels of one solve over all tiles
 void set_solve_skip(int mask, int only_tile);  // profiling aid (hddm_time_solve only)
+void set_solve_pdl(bool on);                  // programmatic dependent launch of the chains
 
 // ------------------------------------------------------------------ factor
 struct FactorArgs {

@@ -47,6 +47,16 @@ constexpr int kUF = HDDM_UF;  // forward gathers in flight per lane
 constexpr int kUB = HDDM_UB;  // backward rows in flight per lane
 constexpr unsigned kFull = 0xffffffffu;
 
+// Programmatic dependent launch: every solve kernel lets its successor in the
+// stream launch as soon as all of its CTAs are resident (trigger), does its
+// static setup (tile records, item lists, activity flags -- all written before
+// the solve), and waits for its predecessor's completion before touching any
+// vector or writing anything.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // one lane of a tile-group launch: warp w serves tile w / wpt of the group
 // (wpt = warps per tile for this level), items (w % wpt) * R + r
 struct TL {
@@ -191,7 +201,9 @@ __device__ __forceinline__ cplx bw_gather(const cplx* __restrict__ vals, const B
 
 // identity ring rows: x = b (thread per (position, member))
 __global__ void __launch_bounds__(kThreads) k_ring(SolveArgs A, TileArg T) {
+  pdl_trigger();
   const TL L = tile_lane(A, T, A.nring);
+  pdl_wait();
   if (!L.act) return;
   const long long p = vat(L, int(L.it));
   A.X[p] = A.B[p];
@@ -204,8 +216,10 @@ constexpr int kBand = 6;
 
 __global__ void __launch_bounds__(kThreads) k_fwd_leaf(SolveArgs A, TileArg T, const int2* items,
                                                        int nitem) {
+  pdl_trigger();
   const TL L = tile_lane(A, T, nitem);
   const long long it = L.it;
+  pdl_wait();
   if (!L.act) return;
   const DevSn sn = A.sn[items[it].x];
   const cplx* vals = A.vals + (long long)L.c * A.nvals;
@@ -233,9 +247,11 @@ __global__ void __launch_bounds__(kThreads) k_fwd_leaf(SolveArgs A, TileArg T, c
 // rec[item] = (position, run length, run offset lo, hi).
 __global__ void __launch_bounds__(kThreads) k_fwd_pull(SolveArgs A, TileArg T, const int4* rec,
                                                        int nitem) {
+  pdl_trigger();
   const TL L = tile_lane(A, T, nitem);
   const long long it = L.it;
   const bool live = L.act;
+  pdl_wait();
   int4 R = make_int4(0, 0, 0, 0);
   cplx acc = cmk(0, 0);
   if (live) {
@@ -254,9 +270,11 @@ __global__ void __launch_bounds__(kThreads) k_fwd_pull(SolveArgs A, TileArg T, c
 // separator rows, forward diagonal: X[i] = Y[i] + sum_{j<i} Linv[i][j] Y[j]
 __global__ void __launch_bounds__(kThreads) k_fwd_diag(SolveArgs A, TileArg T, const int2* items,
                                                        int nitem) {
+  pdl_trigger();
   const TL L = tile_lane(A, T, nitem);
   const long long it = L.it;
   const bool live = L.act;
+  pdl_wait();
   int2 item = make_int2(0, 0);
   long long y0 = 0;
   cplx acc = cmk(0, 0), acc2 = cmk(0, 0);
@@ -291,8 +309,10 @@ __global__ void __launch_bounds__(kThreads) k_fwd_diag(SolveArgs A, TileArg T, c
 template <bool TO_X>
 __global__ void __launch_bounds__(kThreads) k_bwd_pull(SolveArgs A, TileArg T, const int2* items,
                                                        int nitem) {
+  pdl_trigger();
   const TL L = tile_lane(A, T, nitem);
   const long long it = L.it;
+  pdl_wait();
   if (!L.act) return;
   const int2 item = items[it];
   const DevSn sn = A.sn[item.x];
@@ -309,8 +329,10 @@ __global__ void __launch_bounds__(kThreads) k_bwd_pull(SolveArgs A, TileArg T, c
 // (thread per (column, member))
 __global__ void __launch_bounds__(kThreads) k_bwd_diag(SolveArgs A, TileArg T, const int2* items,
                                                        int nitem) {
+  pdl_trigger();
   const TL L = tile_lane(A, T, nitem);
   const long long it = L.it;
+  pdl_wait();
   if (!L.act) return;
   const int2 item = items[it];
   const DevSn sn = A.sn[item.x];
@@ -342,6 +364,7 @@ template <bool DIAG>
 __global__ void __launch_bounds__(kThreads) k_bwd_split(SolveArgs A, TileArg T, const int2* items,
                                                         int nitem) {
   __shared__ cplx part[8][32];
+  pdl_trigger();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ti = blockIdx.x / nitem;  // CTA per (tile, column group)
   TL L;
@@ -356,6 +379,7 @@ __global__ void __launch_bounds__(kThreads) k_bwd_split(SolveArgs A, TileArg T, 
   const bool ok = L.act && j < sn.n;
   const cplx* vals = A.vals + (long long)L.c * A.nvals;
   cplx acc = cmk(0, 0);
+  pdl_wait();
   if (ok) {
     if (DIAG) {
       const cplx* Linv = vals + sn.diag_off;
@@ -397,6 +421,7 @@ __global__ void __launch_bounds__(kStageThreads) k_bwd_stage(SolveArgs A, TileAr
                                                              const int4* chunks, int nchunk,
                                                              int RC, int CWmax) {
   extern __shared__ __align__(16) unsigned char smem[];
+  pdl_trigger();
   const int ti = blockIdx.x / nchunk;
   const int4 ch = chunks[blockIdx.x - ti * nchunk];  // (supernode, j0, j1, -)
   const TileRec* rec = T.rec + ti;
@@ -423,6 +448,7 @@ __global__ void __launch_bounds__(kStageThreads) k_bwd_stage(SolveArgs A, TileAr
   cplx acc[kMaxQ];
 #pragma unroll
   for (int q = 0; q < kMaxQ; ++q) acc[q] = cmk(0, 0);
+  pdl_wait();
   for (int k0 = 0; k0 < nre; k0 += RC) {
     const int kc = min(RC, nre - k0);
     for (int kk = tid; kk < kc; kk += kStageThreads) rd[kk] = rows[k0 + kk];
@@ -493,8 +519,10 @@ __global__ void __launch_bounds__(kStageThreads) k_bwd_stage(SolveArgs A, TileAr
 // next kBand pending w values. Thread per (leaf, member).
 __global__ void __launch_bounds__(kThreads) k_bwd_leaf(SolveArgs A, TileArg T, const int2* items,
                                                        int nitem) {
+  pdl_trigger();
   const TL L = tile_lane(A, T, nitem);
   const long long it = L.it;
+  pdl_wait();
   if (!L.act) return;
   const DevSn sn = A.sn[items[it].x];
   const cplx* vals = A.vals + (long long)L.c * A.nvals;
@@ -522,6 +550,28 @@ __global__ void __launch_bounds__(kThreads) k_bwd_leaf(SolveArgs A, TileArg T, c
 int solve_launch_count(const SolvePlan& P) {
   return int(P.groups.size()) * (4 + 2 * int(P.fwd.size()) + 2 * int(P.bwd.size()));
 }
+
+static bool g_pdl = false;
+
+// launch with programmatic stream serialization (see pdl_trigger / pdl_wait)
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                       cudaStream_t st, Args... args) {
+  if (grid == 0) return;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, args...);
+}
+
+void set_solve_pdl(bool on) { g_pdl = on; }
 
 static unsigned blocks_for(long long threads) {
   return unsigned((threads + kThreads - 1) / kThreads);
@@ -566,8 +616,8 @@ static void launch_bwd_stage(const SolveArgs& A, const TileArg& T, const SolveLe
   const int rowb = (T.M + L.cw_max + 1) * int(sizeof(cplx));
   const int RC = std::max(1, (kBudget - kStageThreads * int(sizeof(cplx))) / rowb);
   const size_t smem = size_t(RC) * rowb + kStageThreads * sizeof(cplx);
-  k_bwd_stage<TO_X><<<unsigned((long long)T.ntile * L.nchunk4), kStageThreads, smem, st>>>(
-      A, T, L.d_chunks4, L.nchunk4, RC, L.cw_max);
+  launch_pdl(k_bwd_stage<TO_X>, unsigned((long long)T.ntile * L.nchunk4), kStageThreads, smem, st,
+             A, T, (const int4*)L.d_chunks4, L.nchunk4, RC, L.cw_max);
 }
 
 // one tile group's full solve on one stream
@@ -577,18 +627,24 @@ void launch_solve_group(const SolveArgs& A, const SolvePlan& P, int g, cudaStrea
   const TileArg T1 = with_shape(P.groups[g], 1);  // thread per (item, member)
   const long long nt = T1.ntile;
   auto blocks = [nt](long long items, int R) { return blocks_for(nt * ((items + R - 1) / R) * 32); };
-  if (!(skip & 1)) k_ring<<<blocks(A.nring, T1.R), kThreads, 0, st>>>(A, T1);
-  const SolveLevel& FL = P.fwd_leaf;
-  if (!(skip & 2))
-    k_fwd_leaf<<<blocks(FL.nitem, T1.R), kThreads, 0, st>>>(A, T1, FL.d_items, FL.nitem);
-  for (const auto& L : P.fwd) {
+  // sparse RHS (steps >= 2): X was cleared; ring rows and patch-free subtrees stay 0
+  const bool sp = A.sparse_rhs && P.has_sparse;
+  if (!(skip & 1) && !sp) k_ring<<<blocks(A.nring, T1.R), kThreads, 0, st>>>(A, T1);
+  const SolveLevel& FL = sp ? P.fwd_leaf_sp : P.fwd_leaf;
+  if (!(skip & 2) && FL.nitem > 0)
+    launch_pdl(k_fwd_leaf, blocks(FL.nitem, T1.R), kThreads, 0, st, A, T1, (const int2*)FL.d_items,
+               FL.nitem);
+  for (const auto& L : (sp ? P.fwd_sp : P.fwd)) {
+    if (L.nitem == 0) continue;
     if (!(skip & 4)) {
       const TileArg Tp = with_shape(T1, fwd_lanes(T1.M, L.avg_run));
-      k_fwd_pull<<<blocks(L.nitem, Tp.R), kThreads, 0, st>>>(A, Tp, L.d_rec, L.nitem);
+      launch_pdl(k_fwd_pull, blocks(L.nitem, Tp.R), kThreads, 0, st, A, Tp, (const int4*)L.d_rec,
+                 L.nitem);
     }
     if (!(skip & 8)) {
       const TileArg Td = with_shape(T1, fwd_lanes(T1.M, L.avg_diag));
-      k_fwd_diag<<<blocks(L.nitem, Td.R), kThreads, 0, st>>>(A, Td, L.d_items, L.nitem);
+      launch_pdl(k_fwd_diag, blocks(L.nitem, Td.R), kThreads, 0, st, A, Td, (const int2*)L.d_items,
+                 L.nitem);
     }
   }
   for (const auto& L : P.bwd) {
@@ -600,25 +656,31 @@ void launch_solve_group(const SolveArgs& A, const SolvePlan& P, int g, cudaStrea
     } else if (P.staged)
       launch_bwd_stage<false>(A, T1, L, st);
     else if (L.split_rows && has_grp)
-      k_bwd_split<false><<<gs, kThreads, 0, st>>>(A, T1, grp->second.second, grp->second.first);
+      launch_pdl(k_bwd_split<false>, gs, kThreads, 0, st, A, T1, (const int2*)grp->second.second,
+                 grp->second.first);
     else
-      k_bwd_pull<false><<<blocks(L.nitem, T1.R), kThreads, 0, st>>>(A, T1, L.d_items, L.nitem);
+      launch_pdl(k_bwd_pull<false>, blocks(L.nitem, T1.R), kThreads, 0, st, A, T1,
+                 (const int2*)L.d_items, L.nitem);
     if (skip & 32) {
     } else if (L.split_diag && has_grp)
-      k_bwd_split<true><<<gs, kThreads, 0, st>>>(A, T1, grp->second.second, grp->second.first);
+      launch_pdl(k_bwd_split<true>, gs, kThreads, 0, st, A, T1, (const int2*)grp->second.second,
+                 grp->second.first);
     else
-      k_bwd_diag<<<blocks(L.nitem, T1.R), kThreads, 0, st>>>(A, T1, L.d_items, L.nitem);
+      launch_pdl(k_bwd_diag, blocks(L.nitem, T1.R), kThreads, 0, st, A, T1, (const int2*)L.d_items,
+                 L.nitem);
   }
   const SolveLevel& BC = P.bwd_leafcol;
   if (!(skip & 64)) {
     if (P.staged)
       launch_bwd_stage<true>(A, T1, BC, st);
     else
-      k_bwd_pull<true><<<blocks(BC.nitem, T1.R), kThreads, 0, st>>>(A, T1, BC.d_items, BC.nitem);
+      launch_pdl(k_bwd_pull<true>, blocks(BC.nitem, T1.R), kThreads, 0, st, A, T1,
+                 (const int2*)BC.d_items, BC.nitem);
   }
   const SolveLevel& BL = P.bwd_leaf;
   if (!(skip & 128))
-    k_bwd_leaf<<<blocks(BL.nitem, T1.R), kThreads, 0, st>>>(A, T1, BL.d_items, BL.nitem);
+    launch_pdl(k_bwd_leaf, blocks(BL.nitem, T1.R), kThreads, 0, st, A, T1, (const int2*)BL.d_items,
+               BL.nitem);
 }
 
 }  // namespace hddm

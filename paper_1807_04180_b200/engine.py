@@ -141,6 +141,7 @@ def load_library(path: str = LIB_PATH):
         "hddm_nd_order": (C.c_int, [C.c_int, C.c_int, ip]),
         "hddm_footprint": (C.c_int, [vp, P(C.c_long), P(C.c_long), P(C.c_long)]),
         "hddm_symbolic_stats": (C.c_int, [C.c_int, C.c_int, P(C.c_long), P(C.c_long), ip, ip]),
+        "hddm_fwd_entries": (C.c_int, [vp, P(C.c_longlong), P(C.c_longlong)]),
         "hddm_set_timing": (C.c_int, [vp, C.c_int]),
         "hddm_stage_times": (C.c_int, [vp, dp, P(C.c_longlong), C.c_int, ip]),
         "hddm_launch_count": (C.c_longlong, [vp]),
@@ -412,6 +413,12 @@ class DdmEngine:
         m, n = C.c_double(), C.c_int()
         self._check(self.lib.hddm_refine_stats(self.h, C.byref(m), C.byref(n)))
         return m.value, n.value
+
+    def fwd_entries(self):
+        """(full, sparse-RHS) factor entries of one class's forward sweep."""
+        a, b = C.c_longlong(), C.c_longlong()
+        self._check(self.lib.hddm_fwd_entries(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def time_solve(self, reps: int = 10) -> float:
         """Average device ms of one batched solve stage (steady state)."""
