@@ -631,12 +631,13 @@ void hddm_engine::build_plan() {
       }
     }
   }
+  static const int stage_cw = std::getenv("HDDM_STAGE_CW") ? std::atoi(std::getenv("HDDM_STAGE_CW")) : 32;
   auto chunks4 = [&](SolveLevel& L, const std::vector<int>& sns) {
     std::vector<int4> ch;
     int cw = 0;
     for (int s : sns)
-      for (int j = 0; j < Y.sn[s].n; j += 32) {
-        const int j1 = std::min(Y.sn[s].n, j + 32);
+      for (int j = 0; j < Y.sn[s].n; j += stage_cw) {
+        const int j1 = std::min(Y.sn[s].n, j + stage_cw);
         ch.push_back(make_int4(s, j, j1, 0));
         cw = std::max(cw, j1 - j);
       }

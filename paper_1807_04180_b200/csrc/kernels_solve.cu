@@ -414,7 +414,13 @@ __global__ void __launch_bounds__(kThreads) k_bwd_split(SolveArgs A, TileArg T, 
 // row chunk -- then every (column, member) pair accumulates from shared memory.
 // Pairs below the CTA size split the rows S ways (fixed-order combine).
 // w_j = Dinv[j] X[j] - sum_rows L[r][j] X[dst r] into Y (X for leaf columns).
-constexpr int kStageThreads = 128;
+#ifndef HDDM_STAGE_THREADS
+#define HDDM_STAGE_THREADS 128
+#endif
+#ifndef HDDM_STAGE_KB
+#define HDDM_STAGE_KB 24  // measured best at config 4 (20-24 KB: 8 CTAs per SM)
+#endif
+constexpr int kStageThreads = HDDM_STAGE_THREADS;
 
 template <bool TO_X>
 __global__ void __launch_bounds__(kStageThreads) k_bwd_stage(SolveArgs A, TileArg T,
@@ -444,7 +450,7 @@ __global__ void __launch_bounds__(kStageThreads) k_bwd_stage(SolveArgs A, TileAr
   const int P = CW * M;                                  // (column, member) pairs
   const int S = P >= kStageThreads ? 1 : kStageThreads / P;  // row splits
   const int pp = tid % P, sp = tid / P;  // split mode: pair, row split
-  constexpr int kMaxQ = 8;  // pairs per thread (P <= kMaxQ * 128)
+  constexpr int kMaxQ = 1024 / kStageThreads;  // pairs per thread (P <= 32 x 32)
   cplx acc[kMaxQ];
 #pragma unroll
   for (int q = 0; q < kMaxQ; ++q) acc[q] = cmk(0, 0);
@@ -584,9 +590,12 @@ static int pow2_floor(long v) {
 }
 
 // lanes per output for a forward pull/diagonal level with mean inner length avg
+// (defaults measured best at config 4; tuning knobs HDDM_FWD_DIV / HDDM_FWD_WIDE)
 static int fwd_lanes(int M, long avg) {
-  if (M == 1) return std::max(1, std::min(32, pow2_floor(avg / 4)));
-  if (avg > 128) return std::max(1, pow2_floor(32 / M));
+  static const long div = std::getenv("HDDM_FWD_DIV") ? std::atol(std::getenv("HDDM_FWD_DIV")) : 16;
+  static const long wide = std::getenv("HDDM_FWD_WIDE") ? std::atol(std::getenv("HDDM_FWD_WIDE")) : 16;
+  if (M == 1) return std::max(1, std::min(32, pow2_floor(avg / div)));
+  if (avg > wide) return std::max(1, pow2_floor(32 / M));
   return 1;
 }
 
@@ -612,7 +621,7 @@ void set_solve_skip(int mask, int only_tile) {
 template <bool TO_X>
 static void launch_bwd_stage(const SolveArgs& A, const TileArg& T, const SolveLevel& L,
                              cudaStream_t st) {
-  constexpr int kBudget = 48 * 1024;
+  constexpr int kBudget = HDDM_STAGE_KB * 1024;  // staging buffer per CTA
   const int rowb = (T.M + L.cw_max + 1) * int(sizeof(cplx));
   const int RC = std::max(1, (kBudget - kStageThreads * int(sizeof(cplx))) / rowb);
   const size_t smem = size_t(RC) * rowb + kStageThreads * sizeof(cplx);
