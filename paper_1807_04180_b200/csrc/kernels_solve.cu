@@ -36,7 +36,10 @@ namespace hddm {
 
 namespace {
 
-constexpr int kThreads = 256;
+#ifndef HDDM_SOLVE_THREADS
+#define HDDM_SOLVE_THREADS 128  // measured best at config 4 (64-512 within 5%)
+#endif
+constexpr int kThreads = HDDM_SOLVE_THREADS;
 #ifndef HDDM_UF
 #define HDDM_UF 4
 #endif
@@ -360,10 +363,12 @@ __global__ void __launch_bounds__(kThreads) k_bwd_diag(SolveArgs A, TileArg T, c
 // the 8 warps split the inner range, partial sums combined in fixed warp order
 // (top levels: few columns, long row lists / inverse columns). items: the
 // group's first column.
+constexpr int kSplitWarps = 8;  // k_bwd_split CTA: 8 warps share one column group
+
 template <bool DIAG>
-__global__ void __launch_bounds__(kThreads) k_bwd_split(SolveArgs A, TileArg T, const int2* items,
+__global__ void __launch_bounds__(kSplitWarps * 32) k_bwd_split(SolveArgs A, TileArg T, const int2* items,
                                                         int nitem) {
-  __shared__ cplx part[8][32];
+  __shared__ cplx part[kSplitWarps][32];
   pdl_trigger();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ti = blockIdx.x / nitem;  // CTA per (tile, column group)
@@ -384,19 +389,19 @@ __global__ void __launch_bounds__(kThreads) k_bwd_split(SolveArgs A, TileArg T, 
     if (DIAG) {
       const cplx* Linv = vals + sn.diag_off;
       const SVec<const cplx> y{A.Y + vat(L, sn.c0), L.m};
-      for (int i = j + 1 + warp; i < sn.n; i += 8)
+      for (int i = j + 1 + warp; i < sn.n; i += kSplitWarps)
         cfma(acc, ldf(Linv + (long long)i * (i - 1) / 2 + j), y[i]);
     } else {
       const BwRow* rows = A.bw + A.bw_ptr[item.x];
       const int nr = rows_upto(rows, A.bw_ptr[item.x + 1] - A.bw_ptr[item.x], j);
-      acc = bw_gather<kUB>(vals, rows, warp, nr, 8, j, A.X + L.cb, L.m);
+      acc = bw_gather<kUB>(vals, rows, warp, nr, kSplitWarps, j, A.X + L.cb, L.m);
     }
   }
   part[warp][lane] = acc;
   __syncthreads();
   if (warp == 0 && ok) {
     cplx sum = part[0][lane];
-    for (int w = 1; w < 8; ++w) sum = cadd(sum, part[w][lane]);
+    for (int w = 1; w < kSplitWarps; ++w) sum = cadd(sum, part[w][lane]);
     const long long p = vat(L, sn.c0 + j);
     if (DIAG)
       A.X[p] = cadd(A.Y[p], sum);
@@ -665,14 +670,14 @@ void launch_solve_group(const SolveArgs& A, const SolvePlan& P, int g, cudaStrea
     } else if (P.staged)
       launch_bwd_stage<false>(A, T1, L, st);
     else if (L.split_rows && has_grp)
-      launch_pdl(k_bwd_split<false>, gs, kThreads, 0, st, A, T1, (const int2*)grp->second.second,
+      launch_pdl(k_bwd_split<false>, gs, kSplitWarps * 32, 0, st, A, T1, (const int2*)grp->second.second,
                  grp->second.first);
     else
       launch_pdl(k_bwd_pull<false>, blocks(L.nitem, T1.R), kThreads, 0, st, A, T1,
                  (const int2*)L.d_items, L.nitem);
     if (skip & 32) {
     } else if (L.split_diag && has_grp)
-      launch_pdl(k_bwd_split<true>, gs, kThreads, 0, st, A, T1, (const int2*)grp->second.second,
+      launch_pdl(k_bwd_split<true>, gs, kSplitWarps * 32, 0, st, A, T1, (const int2*)grp->second.second,
                  grp->second.first);
     else
       launch_pdl(k_bwd_diag, blocks(L.nitem, T1.R), kThreads, 0, st, A, T1, (const int2*)L.d_items,
