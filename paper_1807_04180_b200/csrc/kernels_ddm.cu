@@ -100,41 +100,6 @@ void launch_flags(const StepArgs& A, int ncls, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------ gather sources
-namespace {
-
-// transfer_beta (partition.cpp:131-152)
-__device__ __forceinline__ double tbeta(int d, const DevSub& T, int nov, int p, int q) {
-  const bool fromL = d == 1 || d == 5 || d == 7;  // Right, DownRight, UpRight
-  const bool fromR = d == 0 || d == 4 || d == 6;  // Left, DownLeft, UpLeft
-  const bool fromB = d == 3 || d == 6 || d == 7;  // Up, UpLeft, UpRight
-  const bool fromT = d == 2 || d == 4 || d == 5;  // Down, DownLeft, DownRight
-  double b = 1.0;
-  if (fromL) b = beta0(double(p - T.cx0 - 1) / nov);
-  if (fromR) b = beta0(double(T.cx1 - 1 - p) / nov);
-  double c = 1.0;
-  if (fromB) c = beta0(double(q - T.cy0 - 1) / nov);
-  if (fromT) c = beta0(double(T.cy1 - 1 - q) / nov);
-  if ((fromL || fromR) && (fromB || fromT)) return b * c;
-  return (fromL || fromR) ? b : c;
-}
-
-// transfer_patch (transfer.cpp:7-62): is global node (P,Q) in direction d's patch
-__device__ __forceinline__ bool in_patch(int d, const DevSub& T, int wnx, int wny, int nov,
-                                         int P, int Q) {
-  int p0 = T.wx0 + 1, p1 = T.wx0 + wnx - 2, q0 = T.wy0 + 1, q1 = T.wy0 + wny - 2;
-  const bool fromL = d == 1 || d == 5 || d == 7;
-  const bool fromR = d == 0 || d == 4 || d == 6;
-  const bool fromB = d == 3 || d == 6 || d == 7;
-  const bool fromT = d == 2 || d == 4 || d == 5;
-  if (fromL) { p0 = max(p0, T.cx0 + 1); p1 = min(p1, T.cx0 + 1 + nov); }
-  if (fromR) { p0 = max(p0, T.cx1 - 1 - nov); p1 = min(p1, T.cx1 - 1); }
-  if (fromB) { q0 = max(q0, T.cy0 + 1); q1 = min(q1, T.cy0 + 1 + nov); }
-  if (fromT) { q0 = max(q0, T.cy1 - 1 - nov); q1 = min(q1, T.cy1 - 1); }
-  return P >= p0 && P <= p1 && Q >= q0 && Q <= q1;
-}
-
-}  // namespace
-
 // Right-hand side assembly in two passes (restrict_owned + add_transfer +
 // scale_rhs, ddm.cpp:183-205, transfer.cpp:64-88, discretize.cpp:162-172):
 //  (1) every window node: B = J * f_owned (step 1) or 0; ring rows 0;
@@ -164,7 +129,10 @@ __global__ void __launch_bounds__(256) k_rhs_base(StepArgs A) {
   A.B[e] = v;
 }
 
-__global__ void __launch_bounds__(256) k_rhs_transfer(StepArgs A) {
+#ifndef HDDM_XFER_MINB
+#define HDDM_XFER_MINB 3  // register cap for occupancy: measured -8% per step with the check
+#endif
+__global__ void __launch_bounds__(256, HDDM_XFER_MINB) k_rhs_transfer(StepArgs A) {
   const int t = blockIdx.y;
   if (A.zc[t]) return;
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
@@ -242,7 +210,10 @@ void launch_gather(const StepArgs& A, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------ accumulate
-__global__ void __launch_bounds__(256) k_accumulate(StepArgs A) {
+#ifndef HDDM_ACC_MINB
+#define HDDM_ACC_MINB 1
+#endif
+__global__ void __launch_bounds__(256, HDDM_ACC_MINB) k_accumulate(StepArgs A) {
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)A.gnx * A.gny) return;
   const int P = int(idx % A.gnx), Q = int(idx / A.gnx);
@@ -310,7 +281,10 @@ __device__ __forceinline__ cplx ax_row(XV X, int pos, int wnx, int wny,
 // bitwise-identical window operators (the class criterion), so the stencil
 // coefficients come from the class representative. Per-member sums combine in
 // fixed thread order.
-__global__ void __launch_bounds__(256) k_check(CheckArgs A) {
+#ifndef HDDM_CHECK_MINB
+#define HDDM_CHECK_MINB 3
+#endif
+__global__ void __launch_bounds__(256, HDDM_CHECK_MINB) k_check(CheckArgs A) {
   __shared__ double sr[256], sb[256];
   const int c = blockIdx.y;
   const int c0 = A.vm.cptr[c], m = A.vm.cptr[c + 1] - c0;
