@@ -140,6 +140,12 @@ struct BwRow {
   int first, dpos;
 };
 
+// forward run segment: value offset (per class), length, first source position
+struct SegRec {
+  long long off;
+  int len, zb;
+};
+
 struct DevSub {
   int i, j, cx0, cx1, cy0, cy1, wx0, wy0;
   int lint, rint, bint, tint;

@@ -18,9 +18,9 @@ struct SolveArgs {
   const long long* run_off;  // per position: incoming run [run_off[p], run_off[p+1])
   const int* seg_ptr;        // per position: segments of the run
   const int2* seg;           // (length, first source position)
-  const int* zidx;           // per run value: source position (structural, all classes)
   const int* bw_ptr;         // per supernode: backward rows
   const BwRow* bw;
+  const SegRec* fseg;  // forward run segments of the plan in use (full or sparse RHS)
   const cplx* vals;    // ncls x nvals
   long long nvals;
   const int* flag;     // per RHS t: active iff (flag[t] != 0) == flag_on
@@ -55,7 +55,7 @@ struct TileArg {
 struct SolveLevel {
   int nitem = 0;
   int2* d_items = nullptr;
-  int4* d_rec = nullptr;    // forward rows: (position, run length, run offset lo, hi)
+  int4* d_rec = nullptr;    // forward rows: (position, first segment, segment count, -)
   long avg_run = 0;         // forward: mean incoming run length
   long avg_diag = 0;        // forward: mean dense-inverse row length
   bool split_rows = false;  // backward pull: a CTA of 8 warps splits long row lists
@@ -74,6 +74,8 @@ struct SolvePlan {
   SolveLevel fwd_leaf_sp;              // the same restricted to subtrees holding transfer-
   std::vector<SolveLevel> fwd_sp;      // patch nodes (steps >= 2; X cleared beforehand)
   bool has_sparse = false;
+  SegRec* d_fseg = nullptr;            // segments referenced by fwd levels' records
+  SegRec* d_fseg_sp = nullptr;         // live segments (active sources) for fwd_sp
   std::vector<SolveLevel> bwd;         // separator columns by depth (pull, then diag)
   SolveLevel bwd_leafcol;              // leaf columns: w = Dinv z - B^T x
   SolveLevel bwd_leaf;                 // leaves: band back-substitution

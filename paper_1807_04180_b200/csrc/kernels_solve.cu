@@ -113,42 +113,29 @@ __device__ __forceinline__ void csub_mul(cplx& acc, cplx l, cplx x) {
   acc.y -= l.x * x.y + l.y * x.x;
 }
 
-// sum_{q = start, start+step, ... < n} L[q] * X[zi[q] * m]; factor values and
-// source indices of the next batch are in flight while the current batch's
-// vector entries are consumed
+// sum over a row's run segments of L[q] * X[(zb + q) * m]: a segment is a
+// contiguous piece of the factor values against consecutive source positions,
+// so no per-element index is loaded; lanes e, e+E, ... stride each segment with
+// U loads of both operands in flight.
 template <int U>
-__device__ __forceinline__ cplx gather_dot(const cplx* __restrict__ L, const int* __restrict__ zi,
-                                           int start, int n, int step, const cplx* __restrict__ X,
-                                           int m) {
+__device__ __forceinline__ cplx seg_dot(const cplx* __restrict__ vals, const SegRec* __restrict__ sg,
+                                        int ns, int e, int E, const cplx* __restrict__ X, int m) {
   cplx acc0 = cmk(0, 0), acc1 = cmk(0, 0);
-  cplx l[U];
-  int ix[U];
+  for (int k = 0; k < ns; ++k) {
+    const SegRec r = sg[k];
+    const cplx* L = vals + r.off;
+    const cplx* Xs = X + (long long)r.zb * m;
+    for (int q0 = e; q0 < r.len; q0 += U * E) {
+      cplx l[U], x[U];
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int q = start + u * step;
-    const bool ok = q < n;
-    l[u] = ok ? ldf(L + q) : cmk(0, 0);
-    ix[u] = ok ? __ldg(zi + q) : -1;
-  }
-  for (int q0 = start; q0 < n; q0 += U * step) {
-    cplx x[U];
+      for (int u = 0; u < U; ++u) {
+        const int q = q0 + u * E;
+        const bool ok = q < r.len;
+        l[u] = ok ? ldf(L + q) : cmk(0, 0);
+        x[u] = ok ? Xs[(long long)q * m] : cmk(0, 0);
+      }
 #pragma unroll
-    for (int u = 0; u < U; ++u) x[u] = ix[u] >= 0 ? X[(long long)ix[u] * m] : cmk(0, 0);
-    cplx ln[U];
-    int ixn[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int q = q0 + (U + u) * step;
-      const bool ok = q < n;
-      ln[u] = ok ? ldf(L + q) : cmk(0, 0);
-      ixn[u] = ok ? __ldg(zi + q) : -1;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) cfma((u & 1) ? acc1 : acc0, l[u], x[u]);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      l[u] = ln[u];
-      ix[u] = ixn[u];
+      for (int u = 0; u < U; ++u) cfma((u & 1) ? acc1 : acc0, l[u], x[u]);
     }
   }
   return cadd(acc0, acc1);
@@ -247,7 +234,7 @@ __global__ void __launch_bounds__(kThreads) k_fwd_leaf(SolveArgs A, TileArg T, c
 }
 
 // separator rows, forward pull: Y[r] = B[r] - run(r) . X[src].
-// rec[item] = (position, run length, run offset lo, hi).
+// rec[item] = (position, first segment in A.fseg, segment count, -).
 __global__ void __launch_bounds__(kThreads) k_fwd_pull(SolveArgs A, TileArg T, const int4* rec,
                                                        int nitem) {
   pdl_trigger();
@@ -259,9 +246,8 @@ __global__ void __launch_bounds__(kThreads) k_fwd_pull(SolveArgs A, TileArg T, c
   cplx acc = cmk(0, 0);
   if (live) {
     R = __ldg(rec + it);
-    const long long r0 = (long long)(unsigned)R.z | ((long long)R.w << 32);
-    acc = gather_dot<kUF>(A.vals + (long long)L.c * A.nvals + r0, A.zidx + r0, L.e, R.y, T.E,
-                        A.X + L.cb, L.m);
+    acc = seg_dot<kUF>(A.vals + (long long)L.c * A.nvals, A.fseg + R.y, R.z, L.e, T.E, A.X + L.cb,
+                       L.m);
   }
   if (T.E > 1) acc = tile_reduce(acc, T, L);
   if (live && L.e == 0) {
@@ -635,14 +621,16 @@ static void launch_bwd_stage(const SolveArgs& A, const TileArg& T, const SolveLe
 }
 
 // one tile group's full solve on one stream
-void launch_solve_group(const SolveArgs& A, const SolvePlan& P, int g, cudaStream_t st) {
+void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStream_t st) {
   const int skip = skip_mask();
   if (g_only >= 0 && g != g_only) return;
   const TileArg T1 = with_shape(P.groups[g], 1);  // thread per (item, member)
   const long long nt = T1.ntile;
   auto blocks = [nt](long long items, int R) { return blocks_for(nt * ((items + R - 1) / R) * 32); };
   // sparse RHS (steps >= 2): X was cleared; ring rows and patch-free subtrees stay 0
-  const bool sp = A.sparse_rhs && P.has_sparse;
+  const bool sp = A0.sparse_rhs && P.has_sparse;
+  SolveArgs A = A0;
+  A.fseg = sp ? P.d_fseg_sp : P.d_fseg;
   if (!(skip & 1) && !sp) k_ring<<<blocks(A.nring, T1.R), kThreads, 0, st>>>(A, T1);
   const SolveLevel& FL = sp ? P.fwd_leaf_sp : P.fwd_leaf;
   if (!(skip & 2) && FL.nitem > 0)
