@@ -151,3 +151,29 @@ def test_cfg4_fullsize_fgmres():
     o = pyoracle.OracleEngine(prob)
     assert rel_l2(z1, o.precondition(r, 2)) <= 1e-10
     e.close()
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_sparse_rhs_forward_skip_is_exact(cfg, monkeypatch):
+    """Steps >= 2 skip the forward subtrees without transfer-patch nodes and the
+    run segments from them (their z is exactly 0). Disabling the skip
+    (HDDM_NO_SPARSE_RHS, read when the plan is built) must give the same sweeps
+    to rounding (the plans may stride their sums differently), the same solve
+    and skip counts, and fewer forward entries read."""
+    from paper_1807_04180_b200.engine import DdmEngine, DdmStats
+    from paper_1807_04180_b200.problems import config
+    prob = config(cfg)
+    r = interior_random(prob, 21)
+    monkeypatch.delenv("HDDM_NO_SPARSE_RHS", raising=False)
+    with DdmEngine(prob) as a:
+        sa = DdmStats()
+        za = a.precondition(r, 6, sa)
+        full, sparse = a.fwd_entries()
+    monkeypatch.setenv("HDDM_NO_SPARSE_RHS", "1")
+    with DdmEngine(prob) as b:
+        sb = DdmStats()
+        zb = b.precondition(r, 6, sb)
+        full_b, sparse_b = b.fwd_entries()
+    assert rel_l2(za, zb) <= 1e-13
+    assert (sa.solves, sa.skipped) == (sb.solves, sb.skipped)
+    assert sparse < full and (full_b, sparse_b) == (full, full)
