@@ -583,7 +583,7 @@ static int pow2_floor(long v) {
 // lanes per output for a forward pull/diagonal level with mean inner length avg
 // (defaults measured best at config 4; tuning knobs HDDM_FWD_DIV / HDDM_FWD_WIDE)
 static int fwd_lanes(int M, long avg) {
-  static const long div = std::getenv("HDDM_FWD_DIV") ? std::atol(std::getenv("HDDM_FWD_DIV")) : 16;
+  static const long div = std::getenv("HDDM_FWD_DIV") ? std::atol(std::getenv("HDDM_FWD_DIV")) : 32;
   static const long wide = std::getenv("HDDM_FWD_WIDE") ? std::atol(std::getenv("HDDM_FWD_WIDE")) : 16;
   if (M == 1) return std::max(1, std::min(32, pow2_floor(avg / div)));
   if (avg > wide) return std::max(1, pow2_floor(32 / M));
@@ -654,8 +654,12 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
     const auto grp = L.groups.find(T1.R);
     const bool has_grp = grp != L.groups.end();
     const unsigned gs = has_grp ? unsigned(nt * grp->second.first) : 0;
+    // staging pays for multi-member tiles; singletons pull per thread (measured)
+    static const int stage_min_m =
+        std::getenv("HDDM_STAGE_MIN_M") ? std::atoi(std::getenv("HDDM_STAGE_MIN_M")) : 2;
+    const bool staged = P.staged && T1.M >= stage_min_m;
     if (skip & 16) {
-    } else if (P.staged)
+    } else if (staged)
       launch_bwd_stage<false>(A, T1, L, st);
     else if (L.split_rows && has_grp)
       launch_pdl(k_bwd_split<false>, gs, kSplitWarps * 32, 0, st, A, T1, (const int2*)grp->second.second,
@@ -673,7 +677,9 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
   }
   const SolveLevel& BC = P.bwd_leafcol;
   if (!(skip & 64)) {
-    if (P.staged)
+    static const int leaf_min_m =
+        std::getenv("HDDM_LEAF_STAGE_MIN_M") ? std::atoi(std::getenv("HDDM_LEAF_STAGE_MIN_M")) : 2;
+    if (P.staged && T1.M >= leaf_min_m)
       launch_bwd_stage<true>(A, T1, BC, st);
     else
       launch_pdl(k_bwd_pull<true>, blocks(BC.nitem, T1.R), kThreads, 0, st, A, T1,
