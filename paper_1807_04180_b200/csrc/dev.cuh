@@ -120,7 +120,7 @@ struct DevSn {
   int kind, c0, n, nrows;
   int blk0, nblk, drow0, parent;
   int child0, child1, extadd0, aent0;
-  int aent1, pad0;
+  int aent1, lw;  // lw: leaf width (leaf band rows start at i-1 / i-lw)
   long long diag_off, dinv_off, front_off;
 };
 

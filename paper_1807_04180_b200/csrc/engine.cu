@@ -358,6 +358,7 @@ void hddm_engine::create(const hddm_problem& p) {
     d.extadd0 = a.extadd0;
     d.aent0 = Y.aent0[s];
     d.aent1 = Y.aent0[s + 1];
+    d.lw = a.kind == 0 ? a.w : 0;
     d.diag_off = a.diag_off;
     d.dinv_off = a.dinv_off;
     d.front_off = a.front_off;
@@ -578,10 +579,19 @@ void hddm_engine::build_plan() {
     L.d_items = upload(v);
     return L;
   };
-  for (const SnNode& nd : Y.sn)  // register-window bound of the leaf band kernels
-    if (nd.kind == 0)
-      for (int i = 0; i < nd.n; ++i)
-        if (i - Y.row_first[nd.drow0 + i] > 6) throw std::runtime_error("leaf band wider than 6");
+  // leaves: w x h boxes in natural order; with the 5-point fill their band rows
+  // start at i-1 (first grid row) / i-w and are stored back to back from
+  // diag_off -- the leaf kernels stream them without row tables
+  for (const SnNode& nd : Y.sn)
+    if (nd.kind == 0) {
+      long off = nd.diag_off;
+      for (int i = 0; i < nd.n; ++i) {
+        const int first = i < nd.w ? (i > 0 ? i - 1 : 0) : i - nd.w;
+        if (Y.row_first[nd.drow0 + i] != first || Y.row_off[nd.drow0 + i] != off || i - first > 6)
+          throw std::runtime_error("leaf band profile differs from the w x h natural-order box");
+        off += i - first;
+      }
+    }
   // member tiles (up to 32 members of one class), grouped by member count M:
   // a group shares every launch (optionally capped at HDDM_GROUP_TILES tiles)
   std::vector<int> Rs;  // distinct columns-per-CTA of the backward split kernels

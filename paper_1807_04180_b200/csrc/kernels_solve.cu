@@ -199,10 +199,15 @@ __global__ void __launch_bounds__(kThreads) k_ring(SolveArgs A, TileArg T) {
   A.X[p] = A.B[p];
 }
 
-// leaves, forward: z_i = b_i - sum_{q in [first_i, i)} L[i][q] z_q. The band is
-// at most kBand wide (checked at setup): the last kBand values live in registers.
-// Thread per (leaf, member): T.E == 1, R = 32 / M leaves per warp.
+// leaves, forward: z_i = b_i - sum_{q in [first_i, i)} L[i][q] z_q. A leaf is a
+// w x h box in natural order: row i stores columns [first_i, i) with first_i =
+// i-1 in the first grid row and i-w after it (checked at setup), rows back to
+// back from diag_off -- so the band streams with pointer arithmetic and the next
+// row's entries and right-hand side are loaded while the current row computes.
+// The last kBand values live in a register window. Thread per (leaf, member).
 constexpr int kBand = 6;
+
+__device__ __forceinline__ int leaf_first(int i, int w) { return i < w ? (i > 0 ? i - 1 : 0) : i - w; }
 
 __global__ void __launch_bounds__(kThreads) k_fwd_leaf(SolveArgs A, TileArg T, const int2* items,
                                                        int nitem) {
@@ -212,24 +217,40 @@ __global__ void __launch_bounds__(kThreads) k_fwd_leaf(SolveArgs A, TileArg T, c
   pdl_wait();
   if (!L.act) return;
   const DevSn sn = A.sn[items[it].x];
-  const cplx* vals = A.vals + (long long)L.c * A.nvals;
+  const cplx* p = A.vals + (long long)L.c * A.nvals + sn.diag_off;  // row 0's entries
   const SVec<const cplx> b{A.B + vat(L, sn.c0), L.m};
   const SVec<cplx> x{A.X + vat(L, sn.c0), L.m};
+  const int w = sn.lw, n = sn.n;
   cplx win[kBand + 1];  // win[d] = z_{i-d}
 #pragma unroll
   for (int d = 0; d <= kBand; ++d) win[d] = cmk(0, 0);
-  for (int i = 0; i < sn.n; ++i) {
-    const int rt = sn.drow0 + i;
-    const int first = A.row_first[rt];
-    const cplx* Lr = vals + A.row_off[rt] - first;  // L[q] for q in [first, i)
-    cplx acc = b[i];
+  // current row's band: lv[d] = L[i][i-d] (0 outside the profile), bv = b_i
+  cplx lv[kBand + 1], bv = n > 0 ? b[0] : cmk(0, 0);
 #pragma unroll
-    for (int d = 1; d <= kBand; ++d)
-      if (i - d >= first) csub_mul(acc, ldf(Lr + i - d), win[d]);
+  for (int d = 0; d <= kBand; ++d) lv[d] = cmk(0, 0);
+  for (int i = 0; i < n; ++i) {
+    const int cnt = i - leaf_first(i, w);  // entries of row i, L[i][i-d] = p[cnt - d]
+    const cplx* pn = p + cnt;              // row i+1
+    cplx ln[kBand + 1], bn = cmk(0, 0);
+    const int cn = (i + 1 < n) ? i + 1 - leaf_first(i + 1, w) : 0;
+#pragma unroll
+    for (int d = 1; d <= kBand; ++d) ln[d] = d <= cn ? ldf(pn + cn - d) : cmk(0, 0);
+    if (i + 1 < n) bn = b[i + 1];
+    if (i == 0) {
+#pragma unroll
+      for (int d = 1; d <= kBand; ++d) lv[d] = d <= cnt ? ldf(p + cnt - d) : cmk(0, 0);
+    }
+    cplx acc = bv;
+#pragma unroll
+    for (int d = 1; d <= kBand; ++d) csub_mul(acc, lv[d], win[d]);
 #pragma unroll
     for (int d = kBand; d >= 2; --d) win[d] = win[d - 1];
     win[1] = acc;
     x[i] = acc;
+#pragma unroll
+    for (int d = 1; d <= kBand; ++d) lv[d] = ln[d];
+    bv = bn;
+    p = pn;
   }
 }
 
@@ -512,8 +533,9 @@ __global__ void __launch_bounds__(kStageThreads) k_bwd_stage(SolveArgs A, TileAr
 }
 
 // leaves, backward band back-substitution on w (held in X): for i = n-1..0:
-// x_i = w_i; w_q -= L[i][q] x_i for q in [first_i, i). Register window of the
-// next kBand pending w values. Thread per (leaf, member).
+// x_i = w_i; w_q -= L[i][q] x_i for q in [first_i, i). Rows streamed from the
+// end of the leaf's band (see k_fwd_leaf), the next row's entries in flight;
+// register window of the next kBand pending w values. Thread per (leaf, member).
 __global__ void __launch_bounds__(kThreads) k_bwd_leaf(SolveArgs A, TileArg T, const int2* items,
                                                        int nitem) {
   pdl_trigger();
@@ -522,24 +544,38 @@ __global__ void __launch_bounds__(kThreads) k_bwd_leaf(SolveArgs A, TileArg T, c
   pdl_wait();
   if (!L.act) return;
   const DevSn sn = A.sn[items[it].x];
-  const cplx* vals = A.vals + (long long)L.c * A.nvals;
+  const int w = sn.lw, n = sn.n;
+  const cplx* base = A.vals + (long long)L.c * A.nvals + sn.diag_off;
+  long long tot = 0;  // entries of the whole band
+  for (int i = 0; i < n; ++i) tot += i - leaf_first(i, w);
+  const cplx* p = base + tot;  // one past row n-1
   const SVec<cplx> x{A.X + vat(L, sn.c0), L.m};
-  const int n = sn.n;
-  cplx w[kBand + 1];  // w[d] = pending w_{i-d}
+  cplx wv[kBand + 1];  // wv[d] = pending w_{i-d}
 #pragma unroll
-  for (int d = 0; d <= kBand; ++d) w[d] = (n - 1 - d >= 0) ? x[n - 1 - d] : cmk(0, 0);
+  for (int d = 0; d <= kBand; ++d) wv[d] = (n - 1 - d >= 0) ? x[n - 1 - d] : cmk(0, 0);
+  cplx lv[kBand + 1];
+  {
+    const int c = n > 0 ? n - 1 - leaf_first(n - 1, w) : 0;
+#pragma unroll
+    for (int d = 1; d <= kBand; ++d) lv[d] = d <= c ? ldf(p - d) : cmk(0, 0);
+    p -= c;  // start of row n-1
+  }
   for (int i = n - 1; i >= 0; --i) {
-    const cplx xi = w[0];
+    const int cn = i > 0 ? i - 1 - leaf_first(i - 1, w) : 0;  // row i-1
+    cplx ln[kBand + 1];
+#pragma unroll
+    for (int d = 1; d <= kBand; ++d) ln[d] = d <= cn ? ldf(p - d) : cmk(0, 0);
+    const cplx nxt = (i - 1 - kBand >= 0) ? x[i - 1 - kBand] : cmk(0, 0);
+    const cplx xi = wv[0];
     x[i] = xi;
-    const int rt = sn.drow0 + i;
-    const int first = A.row_first[rt];
-    const cplx* Lr = vals + A.row_off[rt] - first;
 #pragma unroll
-    for (int d = 1; d <= kBand; ++d)
-      if (i - d >= first) csub_mul(w[d], ldf(Lr + i - d), xi);
+    for (int d = 1; d <= kBand; ++d) csub_mul(wv[d], lv[d], xi);
 #pragma unroll
-    for (int d = 0; d < kBand; ++d) w[d] = w[d + 1];
-    w[kBand] = (i - 1 - kBand >= 0) ? x[i - 1 - kBand] : cmk(0, 0);
+    for (int d = 0; d < kBand; ++d) wv[d] = wv[d + 1];
+    wv[kBand] = nxt;
+#pragma unroll
+    for (int d = 1; d <= kBand; ++d) lv[d] = ln[d];
+    p -= cn;
   }
 }
 
