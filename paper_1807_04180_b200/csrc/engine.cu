@@ -629,6 +629,27 @@ void hddm_engine::build_plan() {
           plan.tiles.push_back(t);
           plan.tile_group.push_back(int(plan.groups.size()));
         }
+        // sub-tiles of 2 members (M even) for the levels with long rows: more
+        // lanes per row and more warps, the factor entries re-read per sub-tile
+        TileArg Sg = G;
+        const int Ms = (M % 2 == 0 && M > 2) ? 2 : 0;
+        if (Ms) {
+          std::vector<TileRec> sub;
+          for (const TileRec& t : part)
+            for (int k0 = 0; k0 < M; k0 += Ms) {
+              TileRec r = t;
+              r.cb = t.cb + k0;
+              for (int k = 0; k < 32; ++k) r.t[k] = t.t[std::min(k0 + k, M - 1)];
+              sub.push_back(r);
+            }
+          Sg.rec = upload(sub);
+          Sg.ntile = int(sub.size());
+          Sg.M = Ms;
+          Sg.R = 32 / Ms;
+        } else {
+          Sg.ntile = 0;
+        }
+        plan.sub.push_back(Sg);
         plan.groups.push_back(G);
       }
     }
@@ -648,6 +669,8 @@ void hddm_engine::build_plan() {
     L.cw_max = cw;
   };
   plan.staged = std::getenv("HDDM_NO_STAGE") == nullptr;
+  if (const char* v = std::getenv("HDDM_SUB_RUN")) plan.sub_run = std::atol(v);
+  if (const char* v = std::getenv("HDDM_SUB_BWD")) plan.sub_bwd_ctas = std::atoi(v);
   set_solve_pdl(std::getenv("HDDM_PDL") != nullptr);  // measured slower at config 4: opt-in
   plan.fwd_leaf = level(leaves);
   plan.bwd_leaf = level(leaves);

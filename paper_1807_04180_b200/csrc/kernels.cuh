@@ -80,6 +80,12 @@ struct SolvePlan {
   SolveLevel bwd_leafcol;              // leaf columns: w = Dinv z - B^T x
   SolveLevel bwd_leaf;                 // leaves: band back-substitution
   std::vector<TileArg> groups;         // tile groups (E, R set per launch)
+  std::vector<TileArg> sub;            // per group: its tiles split in 2-member sub-tiles
+                                       // (ntile 0: none), for the levels with long rows
+  long sub_run = 1L << 40;             // forward levels with mean run above: sub-tiles
+                                       // (measured slower at config 4: HDDM_SUB_RUN opt-in)
+  int sub_bwd_ctas = 128;              // backward staged levels that would launch fewer
+                                       // CTAs use sub-tiles (measured -3 % at config 4)
   std::vector<TileRec> tiles;          // host copy of every tile
   std::vector<int> tile_group;         // group of each tile
   bool staged = true;                  // backward pulls through shared memory

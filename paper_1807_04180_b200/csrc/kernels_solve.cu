@@ -672,8 +672,23 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
   if (!(skip & 2) && FL.nitem > 0)
     launch_pdl(k_fwd_leaf, blocks(FL.nitem, T1.R), kThreads, 0, st, A, T1, (const int2*)FL.d_items,
                FL.nitem);
+  const TileArg& TS = P.sub[g];  // 2-member sub-tiles (ntile 0: none)
+  auto blocks_n = [](long long ntile, long long items, int R) {
+    return blocks_for(ntile * ((items + R - 1) / R) * 32);
+  };
   for (const auto& L : (sp ? P.fwd_sp : P.fwd)) {
     if (L.nitem == 0) continue;
+    if (TS.ntile > 0 && L.avg_run > P.sub_run) {  // long rows: sub-tiles
+      const TileArg Tp = with_shape(TS, fwd_lanes(TS.M, L.avg_run));
+      if (!(skip & 4))
+        launch_pdl(k_fwd_pull, blocks_n(Tp.ntile, L.nitem, Tp.R), kThreads, 0, st, A, Tp,
+                   (const int4*)L.d_rec, L.nitem);
+      const TileArg Td = with_shape(TS, fwd_lanes(TS.M, L.avg_diag));
+      if (!(skip & 8))
+        launch_pdl(k_fwd_diag, blocks_n(Td.ntile, L.nitem, Td.R), kThreads, 0, st, A, Td,
+                   (const int2*)L.d_items, L.nitem);
+      continue;
+    }
     if (!(skip & 4)) {
       const TileArg Tp = with_shape(T1, fwd_lanes(T1.M, L.avg_run));
       launch_pdl(k_fwd_pull, blocks(L.nitem, Tp.R), kThreads, 0, st, A, Tp, (const int4*)L.d_rec,
@@ -694,9 +709,10 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
     static const int stage_min_m =
         std::getenv("HDDM_STAGE_MIN_M") ? std::atoi(std::getenv("HDDM_STAGE_MIN_M")) : 2;
     const bool staged = P.staged && T1.M >= stage_min_m;
+    const bool use_sub = staged && TS.ntile > 0 && (long long)T1.ntile * L.nchunk4 < P.sub_bwd_ctas;
     if (skip & 16) {
     } else if (staged)
-      launch_bwd_stage<false>(A, T1, L, st);
+      launch_bwd_stage<false>(A, use_sub ? with_shape(TS, 1) : T1, L, st);
     else if (L.split_rows && has_grp)
       launch_pdl(k_bwd_split<false>, gs, kSplitWarps * 32, 0, st, A, T1, (const int2*)grp->second.second,
                  grp->second.first);
