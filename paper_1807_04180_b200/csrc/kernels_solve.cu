@@ -618,8 +618,10 @@ static int pow2_floor(long v) {
 
 // lanes per output for a forward pull/diagonal level with mean inner length avg
 // (defaults measured best at config 4; tuning knobs HDDM_FWD_DIV / HDDM_FWD_WIDE)
-static int fwd_lanes(int M, long avg) {
-  static const long div = std::getenv("HDDM_FWD_DIV") ? std::atol(std::getenv("HDDM_FWD_DIV")) : 32;
+static int fwd_lanes(int M, long avg, bool diag = false) {
+  static const long div_pull = std::getenv("HDDM_FWD_DIV") ? std::atol(std::getenv("HDDM_FWD_DIV")) : 32;
+  static const long div_diag = std::getenv("HDDM_DIAG_DIV") ? std::atol(std::getenv("HDDM_DIAG_DIV")) : 4;
+  const long div = diag ? div_diag : div_pull;
   static const long wide = std::getenv("HDDM_FWD_WIDE") ? std::atol(std::getenv("HDDM_FWD_WIDE")) : 16;
   if (M == 1) return std::max(1, std::min(32, pow2_floor(avg / div)));
   if (avg > wide) return std::max(1, pow2_floor(32 / M));
@@ -683,7 +685,7 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
       if (!(skip & 4))
         launch_pdl(k_fwd_pull, blocks_n(Tp.ntile, L.nitem, Tp.R), kThreads, 0, st, A, Tp,
                    (const int4*)L.d_rec, L.nitem);
-      const TileArg Td = with_shape(TS, fwd_lanes(TS.M, L.avg_diag));
+      const TileArg Td = with_shape(TS, fwd_lanes(TS.M, L.avg_diag, true));
       if (!(skip & 8))
         launch_pdl(k_fwd_diag, blocks_n(Td.ntile, L.nitem, Td.R), kThreads, 0, st, A, Td,
                    (const int2*)L.d_items, L.nitem);
@@ -695,7 +697,7 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
                  L.nitem);
     }
     if (!(skip & 8)) {
-      const TileArg Td = with_shape(T1, fwd_lanes(T1.M, L.avg_diag));
+      const TileArg Td = with_shape(T1, fwd_lanes(T1.M, L.avg_diag, true));
       launch_pdl(k_fwd_diag, blocks(L.nitem, Td.R), kThreads, 0, st, A, Td, (const int2*)L.d_items,
                  L.nitem);
     }
