@@ -130,6 +130,7 @@ struct hddm_engine {
   int* d_undo = nullptr;
   int* d_any = nullptr;
   long long* d_nfix = nullptr;
+  int* d_done = nullptr;  // last-block counter of k_finish_init
   // one CUDA graph per step variant (step 1; s >= 2 by s mod 3), each with a
   // conditional WHILE node running the refinement corrections on demand
   cudaStream_t st2 = nullptr;
@@ -141,7 +142,7 @@ struct hddm_engine {
   ForkSet fork_main, fork_body;
   bool per_class_streams = true;
   cudaGraphExec_t step_exec[4] = {};
-  int step_kernels = 0;
+  int step_kernels[4] = {};  // kernels per step graph variant when no correction runs
   // global
   cplx* d_ga = nullptr;
   double* d_k2 = nullptr;
@@ -494,6 +495,8 @@ void hddm_engine::create(const hddm_problem& p) {
   d_undo = dalloc<int>(nsub);
   d_any = dalloc<int>(1);
   d_nfix = dalloc<long long>(1);
+  d_done = dalloc<int>(1);
+  CK(cudaMemsetAsync(d_done, 0, sizeof(int), st));
   CK(cudaMemsetAsync(d_nfix, 0, sizeof(long long), st));
 
   // ---- global data
@@ -1118,8 +1121,11 @@ void hddm_engine::enqueue_step_front(int s, cudaStream_t stream, unsigned long l
     SA.sparse_rhs = 1;
   }
   if (!no_solve) enqueue_solve(SA, stream);
-  launch_check(check_args(d_B, A.Ucur, A.zc, nullptr), stream);
-  if (!no_solve) launch_refine_init(refine_args(d_B, A.Ucur, A.zc, cond), stream);
+  if (no_solve)
+    launch_check(check_args(d_B, A.Ucur, A.zc, nullptr), stream);
+  else
+    launch_check_init(check_args(d_B, A.Ucur, A.zc, nullptr), refine_args(d_B, A.Ucur, A.zc, cond),
+                      d_done, stream);
 }
 
 // The batched solve on `stream`. On the engine stream, every class runs its
@@ -1199,7 +1205,9 @@ void hddm_engine::build_step_graph(int v) {
   CK(cudaGraphDestroy(g));
   // kernels per step when no correction runs: flags, 2 RHS, solve, check (2),
   // refine init, accumulate
-  step_kernels = 1 + 2 + solve_launches() + 2 + 1 + 1;
+  // flags, RHS (base + transfer at step 1; after it B is cleared by a memset),
+  // the solve, check + finish/refine-init, accumulate
+  step_kernels[v] = 1 + (s == 1 ? 2 : 1) + solve_launches() + 2 + 1;
 }
 
 void hddm_engine::run_step(int s) {
@@ -1218,22 +1226,21 @@ void hddm_engine::run_step(int s) {
       enqueue_refine_body(s, st, 0);
     }
     launch_accumulate(A, st);
-    launches += 1 + 2 + solve_launches() + 2 + 1 + 1;
+    launches += 1 + (s == 1 ? 2 : 1) + solve_launches() + 2 + 1;
     last_step = s;
     return;
   }
   const int v = variant_of(s);
   if (!step_exec[v]) build_step_graph(v);
   CK(cudaGraphLaunch(step_exec[v], st));
-  launches += step_kernels;
+  launches += step_kernels[v];
   last_step = s;
 }
 
 // Host-driven refinement (setup-time probe and class-solve taps).
 void hddm_engine::host_refine(const cplx* Bp, cplx* X, const int* zc) {
-  launch_check(check_args(Bp, X, zc, nullptr), st);
   const RefineArgs R = refine_args(Bp, X, zc, 0);
-  launch_refine_init(R, st);
+  launch_check_init(check_args(Bp, X, zc, nullptr), R, d_done, st);
   for (int it = 0; it < 13; ++it) {
     int any = 0;
     CK(cudaMemcpyAsync(&any, d_any, sizeof(int), cudaMemcpyDeviceToHost, st));

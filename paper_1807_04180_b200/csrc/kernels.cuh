@@ -189,6 +189,10 @@ struct CheckArgs {
 };
 void launch_check(const CheckArgs& A, cudaStream_t st);           // partials + per-RHS rel
 void launch_check_partials(const CheckArgs& A, cudaStream_t st);  // partials only
+struct RefineArgs;
+// check partials, then per-RHS rel + refinement init (refine's first pass) in one kernel;
+// `done` is a zeroed device counter
+void launch_check_init(const CheckArgs& A, const RefineArgs& R, int* done, cudaStream_t st);
 
 // Iterative refinement on device (refine, proj/src/sparse.cpp:268-292): per RHS
 // state after the first solve; corrections run inside a conditional WHILE graph

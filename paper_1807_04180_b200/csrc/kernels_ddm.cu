@@ -341,6 +341,57 @@ __global__ void k_check_finish(CheckArgs A, int nsub) {
   }
 }
 
+__device__ __forceinline__ void set_cond(unsigned long long h, int v) {
+  if (h) cudaGraphSetConditional(cudaGraphConditionalHandle(h), unsigned(v));
+}
+
+// check_finish + refine_init in one pass: a warp per right-hand side sums its
+// partials (fixed tree order), records rel for the stopping statistics and the
+// refinement state; the last block to finish sets the WHILE condition.
+__global__ void __launch_bounds__(256) k_finish_init(CheckArgs A, RefineArgs R, int* done) {
+  const int lane = threadIdx.x & 31;
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int need = 0;
+  if (t < A.nsub) {
+    double r2 = 0, b2 = 0;
+    for (int k = lane; k < A.nchunk; k += 32) {
+      r2 += A.part[((long long)t * A.nchunk + k) * 2];
+      b2 += A.part[((long long)t * A.nchunk + k) * 2 + 1];
+    }
+    r2 = warp_sum(r2);
+    b2 = warp_sum(b2);
+    if (lane == 0) {
+      const double rel = b2 > 0 ? sqrt(r2) / sqrt(b2) : 0.0;
+      A.rel[t] = rel;
+      if (rel > 1e-11) atomicAdd(A.refine_flag, 1);
+      atomicMax(reinterpret_cast<unsigned long long*>(A.max_rel),
+                (unsigned long long)__double_as_longlong(rel));
+      need = (!R.zc[t] && b2 > 0 && rel > 1e-11) ? 1 : 0;
+      R.rel_cur[t] = rel;
+      R.need[t] = need;
+      R.ncorr[t] = 0;
+      R.undo[t] = 0;
+    }
+  }
+  const int any = __syncthreads_or(need);
+  if (threadIdx.x == 0) {
+    if (any) atomicOr(R.any, 1);
+    __threadfence();
+    if (atomicAdd(done, 1) == int(gridDim.x) - 1) {  // last block: all flags are in
+      __threadfence();
+      set_cond(R.cond, *reinterpret_cast<volatile int*>(R.any));
+      *done = 0;
+    }
+  }
+}
+
+void launch_check_init(const CheckArgs& A, const RefineArgs& R, int* done, cudaStream_t st) {
+  dim3 g(A.nchunk, A.vm.ncls);
+  k_check<<<g, 256, 0, st>>>(A);
+  cudaMemsetAsync(R.any, 0, sizeof(int), st);
+  k_finish_init<<<unsigned((A.nsub * 32 + 255) / 256), 256, 0, st>>>(A, R, done);
+}
+
 void launch_check_partials(const CheckArgs& A, cudaStream_t st) {
   dim3 g(A.nchunk, A.vm.ncls);
   k_check<<<g, 256, 0, st>>>(A);
@@ -353,9 +404,6 @@ void launch_check(const CheckArgs& A, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------ refinement
-__device__ __forceinline__ void set_cond(unsigned long long h, int v) {
-  if (h) cudaGraphSetConditional(cudaGraphConditionalHandle(h), unsigned(v));
-}
 
 // first pass done: rel[t] from the check partials; start refining RHS above 1e-11
 __global__ void k_refine_init(RefineArgs R) {
