@@ -152,6 +152,8 @@ struct hddm_engine {
   int* d_colcov = nullptr;
   int* d_pnode = nullptr;
   int* d_pmask = nullptr;
+  int* d_xfer_pos = nullptr;
+  double* d_xfer_beta = nullptr;
   int npatch = 0;
   int* d_rowcov = nullptr;
   double* d_part = nullptr;
@@ -557,6 +559,42 @@ void hddm_engine::create(const hddm_problem& p) {
     npatch = int(pn.size());
     d_pnode = upload(pn);
     d_pmask = upload(pm);
+    // per (patch node, direction, stencil point C E W N S): the source-window
+    // position and transfer_beta (partition.cpp:131-152) -- window-local, so
+    // identical for every target window
+    std::vector<int> xpos(size_t(npatch) * 40, -1);
+    std::vector<double> xbeta(size_t(npatch) * 40, 0.0);
+    const int dIx[8] = {+1, -1, 0, 0, +1, -1, +1, -1}, dJx[8] = {0, 0, +1, -1, +1, +1, -1, -1};
+    const int dp[5] = {0, 1, -1, 0, 0}, dq[5] = {0, 0, 0, 1, -1};
+    const int cx0 = S.ext, cx1 = S.ext + S.mcx, cy0 = S.ext, cy1 = S.ext + S.mcy;  // window-local core
+    auto beta0h = [](double t) {
+      if (t <= 0) return 1.0;
+      if (t >= 1) return 0.0;
+      return 1.0 - t * t * t * (10.0 - 15.0 * t + 6.0 * t * t);
+    };
+    for (int u = 0; u < npatch; ++u) {
+      const int lp = pn[u] % wnx, lq = pn[u] / wnx;
+      for (int d = 0; d < 8; ++d) {
+        if (!((pm[u] >> d) & 1)) continue;
+        const int sp = lp - dIx[d] * S.mcx, sq = lq - dJx[d] * S.mcy;
+        const bool fromL = d == 1 || d == 5 || d == 7, fromR = d == 0 || d == 4 || d == 6;
+        const bool fromB = d == 3 || d == 6 || d == 7, fromT = d == 2 || d == 4 || d == 5;
+        for (int k = 0; k < 5; ++k) {
+          const int xp = sp + dp[k], xq = sq + dq[k];
+          const size_t e = (size_t(u) * 8 + d) * 5 + k;
+          if (xp >= 0 && xq >= 0 && xp < wnx && xq < wny) xpos[e] = Y.pinv[xq * wnx + xp];
+          const int p = lp + dp[k], q = lq + dq[k];
+          double b = 1.0;
+          if (fromL) b = beta0h(double(p - cx0 - 1) / S.nov);
+          if (fromR) b = beta0h(double(cx1 - 1 - p) / S.nov);
+          if (fromB) b *= beta0h(double(q - cy0 - 1) / S.nov);
+          if (fromT) b *= beta0h(double(cy1 - 1 - q) / S.nov);
+          xbeta[e] = b;
+        }
+      }
+    }
+    d_xfer_pos = upload(xpos);
+    d_xfer_beta = upload(xbeta);
   }
   d_part = dalloc<double>(2 * size_t(reduce_blocks()));
   d_scal = dalloc<double>(64);
@@ -995,6 +1033,8 @@ StepArgs hddm_engine::step_args(int s, const cplx* f) {
   A.npatch = npatch;
   A.pnode = d_pnode;
   A.pmask = d_pmask;
+  A.xfer_pos = d_xfer_pos;
+  A.xfer_beta = d_xfer_beta;
   A.ih2 = 1.0 / (S.h * S.h);
   A.sub = d_sub;
   A.sa = d_sa;

@@ -127,6 +127,8 @@ struct StepArgs {
   int npatch;            // structural union of the 8 transfer patches (window nodes)
   const int* pnode;
   const int* pmask;      // bit d: node lies in direction d's patch
+  const int* xfer_pos;      // per (patch node, direction, stencil point): source position or -1
+  const double* xfer_beta;  // ... and transfer_beta there
   double ih2;
   const DevSub* sub;
   const cplx* sa;        // per-sub alpha arrays: a1n[wnx] ia1h[wnx] a2n[wny] ia2h[wny]

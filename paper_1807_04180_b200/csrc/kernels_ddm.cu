@@ -164,28 +164,17 @@ __global__ void __launch_bounds__(256, HDDM_XFER_MINB) k_rhs_transfer(StepArgs A
     if ((corner ? A.zp2 : A.zp1)[src]) continue;
     any = true;
     const SVec<const cplx> V = vview(corner ? A.Up2 : A.Up1, A.vm, src);
-    // source-local coordinates of the target node: windows are offset by whole cores
-    const int sp = lp - di * A.mcx, sq = lq - dj * A.mcy;
-    const bool fromL = d == 1 || d == 5 || d == 7, fromR = d == 0 || d == 4 || d == 6;
-    const bool fromB = d == 3 || d == 6 || d == 7, fromT = d == 2 || d == 4 || d == 5;
+    // structural tables: source positions of the 5 stencil points (-1 outside the
+    // source window) and transfer_beta (partition.cpp:131-152) at them -- the same
+    // for every window, since windows are offset by whole cores
+    const int* xp = A.xfer_pos + (u * 8 + d) * 5;
+    const double* xb = A.xfer_beta + (u * 8 + d) * 5;
     cplx w5[5];  // C, E, W, N, S
-    const int dp[5] = {0, 1, -1, 0, 0}, dq[5] = {0, 0, 0, 1, -1};
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
-      const int xp = sp + dp[k], xq = sq + dq[k];
-      cplx v = cmk(0, 0);
-      if (xp >= 0 && xq >= 0 && xp < A.wnx && xq < A.wny) v = V[A.pinv[xq * A.wnx + xp]];
-      if (v.x != 0.0 || v.y != 0.0) {
-        // transfer_beta (partition.cpp:131-152) at the global node
-        const int p = P + dp[k], q = Q + dq[k];
-        double b = 1.0;
-        if (fromL) b = beta0(double(p - T.cx0 - 1) / A.nov);
-        if (fromR) b = beta0(double(T.cx1 - 1 - p) / A.nov);
-        if (fromB) b *= beta0(double(q - T.cy0 - 1) / A.nov);
-        if (fromT) b *= beta0(double(T.cy1 - 1 - q) / A.nov);
-        v = cscale(v, b);
-      }
-      w5[k] = v;
+      const int pos = __ldg(xp + k);
+      const cplx v = pos >= 0 ? V[pos] : cmk(0, 0);
+      w5[k] = cscale(v, __ldg(xb + k));  // beta >= 0: a zero v stays the same zero
     }
     const cplx uc = w5[0];
     // DiscreteOperator::stencil (discretize.hpp:43-54)
