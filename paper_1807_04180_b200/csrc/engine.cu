@@ -117,7 +117,7 @@ struct hddm_engine {
   int* d_act_list = nullptr;
   long long* d_counts = nullptr;
   double* d_part_chk = nullptr;
-  int nchunk = 64;  // residual-check partials per subdomain (position chunks)
+  int nchunk = std::getenv("HDDM_CHECK_CHUNKS") ? std::atoi(std::getenv("HDDM_CHECK_CHUNKS")) : 64;  // residual-check partials per subdomain
   double* d_rel = nullptr;
   int* d_refine = nullptr;
   double* d_maxrel = nullptr;
@@ -153,6 +153,9 @@ struct hddm_engine {
   int* d_pnode = nullptr;
   int* d_pmask = nullptr;
   int* d_xfer_pos = nullptr;
+  int2* d_lpq = nullptr;    // residual-check tables (per factor position)
+  int4* d_nbr = nullptr;
+  double* d_k2c = nullptr;  // per class: window k^2 in factor order
   double* d_xfer_beta = nullptr;
   int npatch = 0;
   int* d_rowcov = nullptr;
@@ -595,6 +598,33 @@ void hddm_engine::create(const hddm_problem& p) {
     }
     d_xfer_pos = upload(xpos);
     d_xfer_beta = upload(xbeta);
+  }
+  // residual check tables (the J-scaled window stencil, discretize.cpp:98-160):
+  // window coordinates and neighbour positions per factor position, k^2 per class
+  {
+    std::vector<int2> lpq(nw);
+    std::vector<int4> nb(nw);
+    for (int pos = 0; pos < nw; ++pos) {
+      const int node = Y.perm[pos];
+      const int lp = node % wnx, lq = node / wnx;
+      const bool ring = lp == 0 || lq == 0 || lp == wnx - 1 || lq == wny - 1;
+      lpq[pos] = make_int2(ring ? -1 : lp, lq);
+      nb[pos] = make_int4(!ring && lq > 1 ? Y.pinv[node - wnx] : -1, !ring && lp > 1 ? Y.pinv[node - 1] : -1,
+                          !ring && lp < wnx - 2 ? Y.pinv[node + 1] : -1,
+                          !ring && lq < wny - 2 ? Y.pinv[node + wnx] : -1);
+    }
+    d_lpq = upload(lpq);
+    d_nbr = upload(nb);
+    std::vector<double> k2c(size_t(ncls) * nw, 0.0);
+    for (int c = 0; c < ncls; ++c) {
+      const Sub& sb = S.subs[S.cls_rep[c]];
+      for (int pos = 0; pos < nw; ++pos) {
+        const int node = Y.perm[pos];
+        const int lp = node % wnx, lq = node / wnx;
+        k2c[size_t(c) * nw + pos] = S.k2[size_t(sb.wy0 + lq) * S.gnx + sb.wx0 + lp];
+      }
+    }
+    d_k2c = upload(k2c);
   }
   d_part = dalloc<double>(2 * size_t(reduce_blocks()));
   d_scal = dalloc<double>(64);
@@ -1098,6 +1128,9 @@ CheckArgs hddm_engine::check_args(const cplx* Bp, const cplx* X, const int* zc,
   C.pinv = d_pinv;
   C.zc = zc;
   C.only = only;
+  C.lpq = d_lpq;
+  C.nbr = d_nbr;
+  C.k2c = d_k2c;
   C.nsub = nsub;
   C.vm = vmap();
   C.B = Bp;
@@ -1128,6 +1161,9 @@ RefineArgs hddm_engine::refine_args(const cplx* Bp, cplx* X, const int* zc,
   R.perm = d_perm;
   R.pinv = d_pinv;
   R.zc = zc;
+  R.lpq = d_lpq;
+  R.nbr = d_nbr;
+  R.k2c = d_k2c;
   R.vm = vmap();
   R.B = Bp;
   R.X = X;

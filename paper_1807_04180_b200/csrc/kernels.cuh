@@ -179,6 +179,9 @@ struct CheckArgs {
   const int* pinv;
   const int* zc;      // per RHS: 1 = inactive
   const int* only;    // if set: process RHS t only when only[t] != 0 (refinement re-checks)
+  const int2* lpq;    // per factor position: window (p, q); p < 0 on the ring
+  const int4* nbr;    // per factor position: S, W, E, N neighbour positions (-1: dropped)
+  const double* k2c;  // per class: k^2 of its window in factor order
   int nsub;
   VMap vm;
   const cplx* B;
@@ -209,6 +212,9 @@ struct RefineArgs {
   const int* perm;
   const int* pinv;
   const int* zc;
+  const int2* lpq;    // as CheckArgs
+  const int4* nbr;
+  const double* k2c;
   VMap vm;            // layout of B, X, R, C
   const cplx* B;
   cplx* X;

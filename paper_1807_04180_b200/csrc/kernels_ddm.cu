@@ -236,15 +236,23 @@ void launch_accumulate(const StepArgs& A, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------ residual check
+#ifndef HDDM_CHECK_MINB
+#define HDDM_CHECK_MINB 3
+#endif
+#ifndef HDDM_CHECK_UNROLL
+#define HDDM_CHECK_UNROLL 1
+#endif
+constexpr int kCheckUnroll = HDDM_CHECK_UNROLL;
 // (A x)_pos for the J-scaled assembled matrix of subdomain t's window
-// (discretize.cpp:98-160): identity ring rows, ring columns dropped.
+// (discretize.cpp:98-160): identity ring rows, ring columns dropped;
+// from structural tables: window coordinates (lp < 0: ring row)
+// and neighbour positions (S, W, E, N; -1 where the coupling is dropped) per
+// factor-order position, k^2 of the class window in factor order
 template <class XV>
-__device__ __forceinline__ cplx ax_row(XV X, int pos, int wnx, int wny,
-                                       int gnx, double ih2, const DevSub& T, const cplx* sa,
-                                       const double* k2g, const int* perm, const int* pinv) {
-  const int node = perm[pos];
-  const int lp = node % wnx, lq = node / wnx;
-  if (lp == 0 || lq == 0 || lp == wnx - 1 || lq == wny - 1) return X[pos];
+__device__ __forceinline__ cplx ax_row_t(XV X, int pos, int wnx, int wny, double ih2,
+                                         const cplx* sa, double k2, int2 lpq, int4 nb) {
+  if (lpq.x < 0) return X[pos];
+  const int lp = lpq.x, lq = lpq.y;
   const cplx* a1n = sa;
   const cplx* ia1h = sa + wnx;
   const cplx* a2n = sa + 2 * wnx;
@@ -253,26 +261,19 @@ __device__ __forceinline__ cplx ax_row(XV X, int pos, int wnx, int wny,
   const cplx ee = cscale(cmul(a2n[lq], ia1h[lp]), ih2);
   const cplx es = cscale(cmul(a1n[lp], ia2h[lq - 1]), ih2);
   const cplx en = cscale(cmul(a1n[lp], ia2h[lq]), ih2);
-  const double k2 = k2g[(long long)(T.wy0 + lq) * gnx + T.wx0 + lp];
   const cplx diag = cadd(cmk(-(ew.x + ee.x + es.x + en.x), -(ew.y + ee.y + es.y + en.y)),
                          cscale(cmul(a1n[lp], a2n[lq]), k2));
-  cplx ax = cmul(diag, X[pos]);
-  if (lq > 1) cfma(ax, es, X[pinv[node - wnx]]);
-  if (lp > 1) cfma(ax, ew, X[pinv[node - 1]]);
-  if (lp < wnx - 2) cfma(ax, ee, X[pinv[node + 1]]);
-  if (lq < wny - 2) cfma(ax, en, X[pinv[node + wnx]]);
+  const cplx xc = X[pos];
+  const cplx xs = nb.x >= 0 ? X[nb.x] : cmk(0, 0), xw = nb.y >= 0 ? X[nb.y] : cmk(0, 0);
+  const cplx xe = nb.z >= 0 ? X[nb.z] : cmk(0, 0), xn = nb.w >= 0 ? X[nb.w] : cmk(0, 0);
+  cplx ax = cmul(diag, xc);
+  if (nb.x >= 0) cfma(ax, es, xs);
+  if (nb.y >= 0) cfma(ax, ew, xw);
+  if (nb.z >= 0) cfma(ax, ee, xe);
+  if (nb.w >= 0) cfma(ax, en, xn);
   return ax;
 }
 
-// Residual partials in storage order: block (chunk, class c); thread t serves
-// member k = t % m at positions t / m, t / m + 256 / m, ... of the chunk, so a
-// warp reads consecutive members (contiguous addresses). Members of a class have
-// bitwise-identical window operators (the class criterion), so the stencil
-// coefficients come from the class representative. Per-member sums combine in
-// fixed thread order.
-#ifndef HDDM_CHECK_MINB
-#define HDDM_CHECK_MINB 3
-#endif
 __global__ void __launch_bounds__(256, HDDM_CHECK_MINB) k_check(CheckArgs A) {
   __shared__ double sr[256], sb[256];
   const int c = blockIdx.y;
@@ -285,16 +286,18 @@ __global__ void __launch_bounds__(256, HDDM_CHECK_MINB) k_check(CheckArgs A) {
   double r2 = 0, b2 = 0;
   if (act) {
     const int rep = A.vm.cmem[c0];
-    const DevSub T = A.sub[rep];
     const cplx* sa = A.sa + (long long)rep * A.sa_stride;
+    const double* k2c = A.k2c + (long long)c * A.nw;
     const SVec<const cplx> X{A.X + A.vm.cbase[c] + k, m};
     const SVec<const cplx> Bv{A.B + A.vm.cbase[c] + k, m};
     const int chunk = (A.nw + A.nchunk - 1) / A.nchunk;
     const int p0 = blockIdx.x * chunk, p1 = min(A.nw, p0 + chunk);
+#pragma unroll kCheckUnroll
     for (int pos = p0 + pi; pos < p1; pos += per) {
       const cplx b = Bv[pos];
       b2 += cnorm2(b);
-      const cplx ax = ax_row(X, pos, A.wnx, A.wny, A.gnx, A.ih2, T, sa, A.k2, A.perm, A.pinv);
+      const cplx ax = ax_row_t(X, pos, A.wnx, A.wny, A.ih2, sa, __ldg(k2c + pos), __ldg(A.lpq + pos),
+                               __ldg(A.nbr + pos));
       r2 += cnorm2(csub(b, ax));
     }
   }
@@ -420,52 +423,28 @@ __global__ void k_refine_init(RefineArgs R) {
   }
 }
 
-// act lists of the RHS still refining, in class order
-__global__ void k_refine_lists(RefineArgs R) {
-  extern __shared__ int sh[];
-  for (int c = threadIdx.x; c < R.ncls; c += blockDim.x) {
-    int cnt = 0;
-    for (int k = R.cls_ptr[c]; k < R.cls_ptr[c + 1]; ++k) cnt += R.need[R.cls_mem[k]];
-    sh[c] = cnt;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int c = 0; c < R.ncls; ++c) {
-      R.act_ptr[c] = acc;
-      acc += sh[c];
-    }
-    R.act_ptr[R.ncls] = acc;
-  }
-  __syncthreads();
-  for (int c = threadIdx.x; c < R.ncls; c += blockDim.x) {
-    int o = R.act_ptr[c];
-    for (int k = R.cls_ptr[c]; k < R.cls_ptr[c + 1]; ++k)
-      if (R.need[R.cls_mem[k]]) R.act_list[o++] = R.cls_mem[k];
-  }
-}
-
 // R = B - A X for the refining RHS
 __global__ void __launch_bounds__(256) k_refine_resid(RefineArgs R) {
   const int t = blockIdx.y;
   if (!R.need[t]) return;
   const int pos = blockIdx.x * blockDim.x + threadIdx.x;
   if (pos >= R.nw) return;
-  const DevSub T = R.sub[t];
+  const int c = R.sub[t].cls;
   const SVec<const cplx> X = vview((const cplx*)R.X, R.vm, t);
-  const cplx ax = ax_row(X, pos, R.wnx, R.wny, R.gnx, R.ih2, T, R.sa + (long long)t * R.sa_stride,
-                         R.k2, R.perm, R.pinv);
+  const cplx ax = ax_row_t(X, pos, R.wnx, R.wny, R.ih2, R.sa + (long long)t * R.sa_stride,
+                           __ldg(R.k2c + (long long)c * R.nw + pos), __ldg(R.lpq + pos),
+                           __ldg(R.nbr + pos));
   const long long p = (X.p - R.X) + (long long)pos * X.s;
   R.R[p] = csub(R.B[p], ax);
 }
 
 // X += C for the refining RHS
 __global__ void __launch_bounds__(256) k_refine_apply(RefineArgs R) {
-  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= R.vm.total) return;
-  int t, pos;
-  vdecode(R.vm, p, t, pos);
+  const int t = blockIdx.y;  // only the refining RHS do work
   if (!R.need[t]) return;
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= R.nw) return;
+  const long long p = __ldg(R.vm.base + t) + (long long)pos * __ldg(R.vm.str + t);
   R.X[p] = cadd(R.X[p], R.C[p]);
 }
 
@@ -507,11 +486,11 @@ __global__ void k_refine_decide(RefineArgs R) {
 }
 
 __global__ void __launch_bounds__(256) k_refine_undo(RefineArgs R) {
-  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= R.vm.total) return;
-  int t, pos;
-  vdecode(R.vm, p, t, pos);
+  const int t = blockIdx.y;
   if (!R.undo[t]) return;  // flag cleared by the next init
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= R.nw) return;
+  const long long p = __ldg(R.vm.base + t) + (long long)pos * __ldg(R.vm.str + t);
   R.X[p] = csub(R.X[p], R.C[p]);
 }
 
@@ -519,18 +498,17 @@ void launch_refine_init(const RefineArgs& R, cudaStream_t st) {
   k_refine_init<<<1, 256, 0, st>>>(R);
 }
 void launch_refine_prep(const RefineArgs& R, cudaStream_t st) {
-  k_refine_lists<<<1, 256, sizeof(int) * R.ncls, st>>>(R);
   dim3 g((R.nw + 255) / 256, R.nsub);
   k_refine_resid<<<g, 256, 0, st>>>(R);
 }
 void launch_refine_apply(const RefineArgs& R, cudaStream_t st) {
-  k_refine_apply<<<unsigned((R.vm.total + 255) / 256), 256, 0, st>>>(R);
+  k_refine_apply<<<dim3((R.nw + 255) / 256, R.nsub), 256, 0, st>>>(R);
 }
 void launch_refine_decide(const RefineArgs& R, cudaStream_t st) {
   k_refine_decide<<<1, 256, 0, st>>>(R);
 }
 void launch_refine_undo(const RefineArgs& R, cudaStream_t st) {
-  k_refine_undo<<<unsigned((R.vm.total + 255) / 256), 256, 0, st>>>(R);
+  k_refine_undo<<<dim3((R.nw + 255) / 256, R.nsub), 256, 0, st>>>(R);
 }
 
 // ------------------------------------------------------------ global stencil
