@@ -141,8 +141,8 @@ struct hddm_engine {
   };
   ForkSet fork_main, fork_body;
   bool per_class_streams = true;
-  cudaGraphExec_t step_exec[4] = {};
-  int step_kernels[4] = {};  // kernels per step graph variant when no correction runs
+  cudaGraphExec_t step_exec[5] = {};
+  int step_kernels[5] = {};  // kernels per step graph variant when no correction runs
   // global
   cplx* d_ga = nullptr;
   double* d_k2 = nullptr;
@@ -1246,8 +1246,10 @@ void hddm_engine::enqueue_refine_body(int s, cudaStream_t stream, unsigned long 
   launch_refine_undo(R, stream);
 }
 
-static int variant_of(int s) { return s == 1 ? 0 : 1 + (s % 3); }
-static int rep_step(int v) { return v == 0 ? 1 : (v == 1 ? 3 : (v == 2 ? 4 : 2)); }
+// step graph variants: 0 = step 1, 4 = step 2 (clears B), 1..3 = steps >= 3 by
+// s mod 3 (the rotation of the U / zero-flag buffers)
+static int variant_of(int s) { return s == 1 ? 0 : (s == 2 ? 4 : 1 + (s % 3)); }
+static int rep_step(int v) { return v == 0 ? 1 : (v == 1 ? 3 : (v == 2 ? 4 : (v == 3 ? 5 : 2))); }
 
 void hddm_engine::build_step_graph(int v) {
   const int s = rep_step(v);
@@ -1288,7 +1290,7 @@ void hddm_engine::build_step_graph(int v) {
 
 void hddm_engine::run_step(int s) {
   if (!step_exec[0] && !std::getenv("HDDM_NO_GRAPHS"))
-    for (int v = 0; v < 4; ++v) build_step_graph(v);  // all variants up front
+    for (int v = 0; v < 5; ++v) build_step_graph(v);  // all variants up front
   static const bool no_graphs = std::getenv("HDDM_NO_GRAPHS") != nullptr;
   if (no_graphs) {
     // direct launches (profiling aid): same kernels, refinement driven from the host

@@ -184,15 +184,22 @@ __global__ void __launch_bounds__(256, HDDM_XFER_MINB) k_rhs_transfer(StepArgs A
     tt = csub(tt, cmul(cS, csub(uc, w5[4])));
     val = csub(val, cadd(cdiv(tt, jac), cscale(uc, k2)));
   }
-  if (any) vview(A.B, A.vm, t)[A.pinv[node]] = cmul(jac, val);
+  // step 1: the base value J f stays where no source contributes; later steps
+  // write every patch node (0 without a contribution), so B stays zero off the
+  // patches after the one clear at step 2
+  if (any)
+    vview(A.B, A.vm, t)[A.pinv[node]] = cmul(jac, val);
+  else if (A.step != 1)
+    vview(A.B, A.vm, t)[A.pinv[node]] = cmk(0, 0);
 }
 
 void launch_gather(const StepArgs& A, cudaStream_t st) {
-  // steps >= 2 see no f: every base value is 0. Right-hand sides of inactive
-  // subdomains are never read, so all of B is cleared at memset speed.
+  // steps >= 2 see no f: every base value is 0. Step 2 clears all of B at memset
+  // speed (right-hand sides of inactive subdomains are never read); from step 3
+  // on B is already zero off the transfer patches, which the transfer rewrites.
   if (A.step == 1)
     k_rhs_base<<<unsigned((A.vm.total + 255) / 256), 256, 0, st>>>(A);
-  else
+  else if (A.step == 2)
     cudaMemsetAsync(A.B, 0, size_t(A.vm.total) * sizeof(cplx), st);
   dim3 g2((A.npatch + 255) / 256, A.nsub);
   k_rhs_transfer<<<g2, 256, 0, st>>>(A);
