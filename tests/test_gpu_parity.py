@@ -157,3 +157,55 @@ def test_cfg2_fgmres_matches_oracle():
     z = e.precondition(f / np.linalg.norm(f), prob.k_steps)
     assert rel_l2(z, zo[0]) <= ITER_TOL
     e.close()
+
+
+@pytest.mark.parametrize("n1,n2", [(1, 1), (3, 1), (1, 3), (3, 2), (5, 4)])
+def test_partition_shapes_match_oracle(n1, n2):
+    """Single-subdomain and non-square partitions (a single window: no
+    transfers; 1-3 member classes; mixed tile groups), layered medium so x and y
+    differ: per-step iterates and residual history, solve/skip counts, the
+    preconditioner on several random inputs, and FGMRES up to its first
+    stagnating iteration (at a near-breakdown the Arnoldi normalisation cancels
+    and last-bit differences in the reduction order steer both codes apart --
+    the reference's own result depends on its summation order there)."""
+    from paper_1807_04180_b200.engine import DdmEngine, DdmStats, FgmresOptions
+    from paper_1807_04180_b200.problems import MEDIUM_LAYERED, small
+    prob = small(24 * n1, n1, n2, 3.0, 3, 6, source=("gaussian", 0.4, 0.55, 0.05)).with_(
+        my=24 * n2, medium_kind=MEDIUM_LAYERED,
+        layers=[(0.0, 0.3, 1.0), (0.3, 0.7, 1.6), (0.7, 1.0, 1.2)])
+    e = DdmEngine(prob)
+    o = pyoracle.OracleEngine(prob)
+    assert [c["members"] for c in e.class_info()] == [c["members"] for c in o.class_info()]
+    f = prob.source_f()
+    st = DdmStats()
+    u = e.solve_iterative(f, 0.0, 5, st)
+    uo, so = o.solve_iterative(f, 0.0, 5)
+    assert rel_l2(u, uo) <= ITER_TOL
+    assert (st.steps, st.solves, st.skipped) == (so.steps, so.solves, so.skipped)
+    for a, b in zip(st.history, so.history):
+        assert abs(a.relres - b[1]) <= 1e-10 * abs(b[1]) + 1e-13
+    rng = np.random.default_rng(n1 * 10 + n2)
+    K = n1 + n2
+    for _ in range(3):  # repeated applications: no state carried between calls
+        r = interior_noise(prob, rng)
+        sa, sb = DdmStats(), pyoracle.Stats()
+        assert rel_l2(e.precondition(r, K, sa), o.precondition(r, K, sb)) <= ITER_TOL
+        assert (sa.solves, sa.skipped) == (sb.solves, sb.skipped)
+    x, res = e.fgmres(f, FgmresOptions(1e-8, 30, 30), K)
+    xo, ro, _, _ = o.fgmres(f, 1e-8, 30, 30, K, keep_z=0)
+    prev = None
+    for a, b in zip(res.history, ro.history):
+        if prev is not None and b >= 0.999 * prev:
+            break  # stagnation: beyond here the comparison is not meaningful
+        assert abs(a - b) <= 1e-8 * abs(b) + 1e-13
+        prev = b
+    if ro.converged and all(ro.history[k] < 0.999 * ro.history[k - 1] for k in range(1, ro.iters)):
+        assert res.iters == ro.iters and rel_l2(x, xo) <= FINAL_TOL
+    e.close()
+
+
+def interior_noise(prob, rng):
+    r = rng.standard_normal(prob.n_global) + 1j * rng.standard_normal(prob.n_global)
+    r = r.reshape(prob.gny, prob.gnx)
+    r[0, :] = r[-1, :] = r[:, 0] = r[:, -1] = 0
+    return r.ravel()
