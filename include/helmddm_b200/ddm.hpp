@@ -6,7 +6,10 @@
 // (types.hpp:58-66).
 #pragma once
 
+#include <chrono>
+#include <cmath>
 #include <complex>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -84,7 +87,11 @@ struct FgmresResult {
   bool converged = false;
   double relres = -1, true_relres = -1;
   std::vector<double> history;
+  std::vector<double> iter_ms;  // host FGMRES only (the device one times the whole solve)
 };
+
+// LinearOp (krylov.hpp:9): y = Op(x) on n complex values
+using LinearOp = std::function<void(const Complex*, Complex*)>;
 
 namespace detail {
 inline void check(int rc, const hddm_engine* e) {
@@ -224,5 +231,134 @@ class DdmEngine {
   DdmConfig cfg_;
   hddm_engine* e_ = nullptr;
 };
+
+// fgmres(n, A, M, b, x, opt) over caller-supplied operators (krylov.hpp:31-33,
+// krylov.cpp:24-133), restated host-side: right-preconditioned flexible GMRES from
+// x = 0, modified Gram-Schmidt, complex Givens rotations, the recursive residual
+// per iteration, cyclic restart with the residual recomputed, stop on tol / a
+// dead column / an invariant subspace, true residual of the returned x. The
+// production path is DdmEngine::fgmres (device-resident, A = apply_global,
+// M = precondition); this form keeps host-lambda callers and lets the caller's
+// FGMRES drive the GPU preconditioner. M may be empty.
+inline FgmresResult fgmres(size_t n, const LinearOp& A, const LinearOp& M,
+                           const std::vector<Complex>& b, std::vector<Complex>& x,
+                           const FgmresOptions& opt) {
+  using clock = std::chrono::steady_clock;
+  auto norm = [n](const std::vector<Complex>& v) {
+    double s = 0;
+    for (size_t t = 0; t < n; ++t) s += std::norm(v[t]);
+    return std::sqrt(s);
+  };
+  FgmresResult res;
+  x.assign(n, Complex(0));
+  const double bnorm = norm(b);
+  if (bnorm == 0) {
+    res.converged = true;
+    res.relres = res.true_relres = 0;
+    return res;
+  }
+  std::vector<Complex> r(b.begin(), b.begin() + long(n));
+  int total = 0;
+  bool stop = false;
+  while (!stop && total < opt.max_iters) {
+    const int m = opt.restart > 0 ? std::min(opt.restart, opt.max_iters - total) : opt.max_iters - total;
+    const double rnorm = norm(r);
+    if (rnorm == 0) {
+      res.converged = true;
+      break;
+    }
+    std::vector<std::vector<Complex>> V(1, r), Z;
+    for (Complex& c : V[0]) c /= rnorm;
+    // column j of the (rotated) Hessenberg matrix: H[j][0..j+1]
+    std::vector<std::vector<Complex>> H;
+    std::vector<Complex> g(static_cast<size_t>(m) + 1, Complex(0));
+    std::vector<Complex> sn(static_cast<size_t>(m));
+    std::vector<double> cs(static_cast<size_t>(m));
+    g[0] = rnorm;
+    int k = 0;
+    for (int j = 0; j < m; ++j) {
+      const auto t0 = clock::now();
+      Z.emplace_back(n);
+      if (M)
+        M(V[size_t(j)].data(), Z.back().data());
+      else
+        Z.back() = V[size_t(j)];
+      std::vector<Complex> w(n);
+      A(Z.back().data(), w.data());
+      H.emplace_back(size_t(j) + 2, Complex(0));
+      std::vector<Complex>& h = H.back();
+      for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt
+        Complex d = 0;
+        const std::vector<Complex>& vi = V[size_t(i)];
+        for (size_t t = 0; t < n; ++t) d += std::conj(vi[t]) * w[t];
+        h[size_t(i)] = d;
+        for (size_t t = 0; t < n; ++t) w[t] -= d * vi[t];
+      }
+      const double hlast = norm(w);
+      h[size_t(j) + 1] = hlast;
+      for (int i = 0; i < j; ++i) {  // earlier rotations on the new column
+        const Complex a = h[size_t(i)], c = h[size_t(i) + 1];
+        h[size_t(i)] = cs[size_t(i)] * a + sn[size_t(i)] * c;
+        h[size_t(i) + 1] = -std::conj(sn[size_t(i)]) * a + cs[size_t(i)] * c;
+      }
+      const Complex a = h[size_t(j)], c = h[size_t(j) + 1];
+      const double tn = std::sqrt(std::norm(a) + std::norm(c));
+      if (tn == 0) {  // dead column: dropped, stop
+        H.pop_back();
+        Z.pop_back();
+        stop = true;
+        break;
+      }
+      if (a == Complex(0)) {
+        cs[size_t(j)] = 0;
+        sn[size_t(j)] = std::conj(c) / std::abs(c);
+      } else {
+        cs[size_t(j)] = std::abs(a) / tn;
+        sn[size_t(j)] = (a / std::abs(a)) * std::conj(c) / tn;
+      }
+      h[size_t(j)] = cs[size_t(j)] * a + sn[size_t(j)] * c;
+      h[size_t(j) + 1] = 0;
+      g[size_t(j) + 1] = -std::conj(sn[size_t(j)]) * g[size_t(j)];
+      g[size_t(j)] = cs[size_t(j)] * g[size_t(j)];
+      ++total;
+      k = j + 1;
+      res.relres = std::abs(g[size_t(j) + 1]) / bnorm;
+      res.history.push_back(res.relres);
+      res.iter_ms.push_back(std::chrono::duration<double, std::milli>(clock::now() - t0).count());
+      if (res.relres <= opt.tol) {
+        res.converged = true;
+        stop = true;
+        break;
+      }
+      if (hlast == 0) {  // invariant subspace
+        stop = true;
+        break;
+      }
+      for (Complex& cv : w) cv /= hlast;
+      V.push_back(std::move(w));
+    }
+    if (k > 0) {  // back substitution on the rotated triangle, x += Z y
+      std::vector<Complex> y(static_cast<size_t>(k));
+      for (int i = k - 1; i >= 0; --i) {
+        Complex s = g[size_t(i)];
+        for (int l = i + 1; l < k; ++l) s -= H[size_t(l)][size_t(i)] * y[size_t(l)];
+        y[size_t(i)] = s / H[size_t(i)][size_t(i)];
+      }
+      for (int l = 0; l < k; ++l)
+        for (size_t t = 0; t < n; ++t) x[t] += y[size_t(l)] * Z[size_t(l)][t];
+    }
+    if (!stop) {  // restart from the explicit residual
+      A(x.data(), r.data());
+      for (size_t t = 0; t < n; ++t) r[t] = b[t] - r[t];
+    }
+  }
+  res.iters = total;
+  std::vector<Complex> ax(n);
+  A(x.data(), ax.data());
+  double s = 0;
+  for (size_t t = 0; t < n; ++t) s += std::norm(b[t] - ax[t]);
+  res.true_relres = std::sqrt(s) / bnorm;
+  return res;
+}
 
 }  // namespace helmddm_b200

@@ -27,3 +27,14 @@ def test_shim_runs_reference_scenarios(tmp_path):
     out = subprocess.run([build(tmp_path)], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "shim ok" in out.stdout
+
+
+def test_host_fgmres_dense_system(tmp_path):
+    """The shim's fgmres(n, A, M, b, x, opt) over LinearOp callbacks (CPU)."""
+    exe = str(tmp_path / "test_fgmres_host")
+    subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "test_fgmres_host.cpp"), "-o", exe],
+                   check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "host fgmres ok" in out.stdout
