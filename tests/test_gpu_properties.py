@@ -177,3 +177,16 @@ def test_sparse_rhs_forward_skip_is_exact(cfg, monkeypatch):
     assert rel_l2(za, zb) <= 1e-13
     assert (sa.solves, sa.skipped) == (sb.solves, sb.skipped)
     assert sparse < full and (full_b, sparse_b) == (full, full)
+
+
+def test_single_subdomain_is_a_direct_solve():
+    """test_ddm.cpp:53-71: a 1x1 partition converges in one sweep with one local
+    solve and relres <= 1e-12."""
+    from paper_1807_04180_b200.engine import DdmEngine, DdmStats
+    from paper_1807_04180_b200.problems import small
+    prob = small(40, 1, 1, 4.0, 4, 8, source=("point", 0.3, 0.6))
+    with DdmEngine(prob) as e:
+        st = DdmStats()
+        e.solve_iterative(prob.source_f(), 1e-10, 5, st)
+        assert st.steps == 1 and st.solves == 1 and st.skipped == 0
+        assert st.converged and st.relres <= 1e-12

@@ -69,3 +69,39 @@ def test_gpu_operators_match_device_fgmres():
     np.testing.assert_allclose(r.history, rd.history, rtol=1e-7, atol=1e-14)
     assert rel_l2(x, xd) <= 1e-8
     e.close()
+
+
+def test_reference_krylov_properties():
+    """test_krylov.cpp:39-202 re-expressed for the host FGMRES."""
+    n = 24
+    rng = np.random.default_rng(41)
+    b = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    # identity: one iteration, exact
+    x, r = fgmres(n, lambda v: v.copy(), None, b, FgmresOptions(1e-12, 50, 0))
+    assert r.iters == 1 and r.converged and np.allclose(x, b)
+    # diagonal: exact within n iterations, true residual recomputed
+    d = 1.0 + np.arange(n)
+    x, r = fgmres(n, lambda v: d * v, None, b, FgmresOptions(1e-13, n, 0))
+    assert r.converged and np.allclose(x, b / d, rtol=1e-11) and r.true_relres <= 1e-12
+    # monotone recursive residual, early exit at tol, honest iteration cap
+    A = np.eye(n) * 3 + 0.4 * (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    x, r = fgmres(n, lambda v: A @ v, None, b, FgmresOptions(1e-6, 100, 0))
+    assert all(h2 <= h1 * (1 + 1e-12) for h1, h2 in zip(r.history, r.history[1:]))
+    assert r.converged and r.relres <= 1e-6 and r.iters == len(r.history)
+    x, r = fgmres(n, lambda v: A @ v, None, b, FgmresOptions(1e-15, 5, 0))
+    assert r.iters == 5 and not r.converged
+    # a variable preconditioner is applied exactly once per iteration
+    calls = [0]
+
+    def M(v):
+        calls[0] += 1
+        return v / np.diag(A) if calls[0] % 2 else v.copy()
+    x, r = fgmres(n, lambda v: A @ v, M, b, FgmresOptions(1e-10, 100, 0))
+    assert r.converged and calls[0] == r.iters
+    # restart still converges; preconditioning helps
+    x, r6 = fgmres(n, lambda v: A @ v, None, b, FgmresOptions(1e-10, 200, 6))
+    assert r6.converged and r6.true_relres <= 1e-9
+    Ainv = np.linalg.inv(A)
+    _, rp = fgmres(n, lambda v: A @ v, lambda v: Ainv @ v, b, FgmresOptions(1e-10, 100, 0))
+    _, ru = fgmres(n, lambda v: A @ v, None, b, FgmresOptions(1e-10, 100, 0))
+    assert rp.iters < ru.iters and rp.iters <= 2
