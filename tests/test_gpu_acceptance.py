@@ -66,3 +66,28 @@ def test_a5_preconditioner_sweeps():
             iters.append(r.iters)
     assert iters[2] * 8 <= iters[0] * 1
     assert iters == [15, 8, 1]  # the reference's counts
+
+
+def test_a2_four_window_exactness():
+    """Point source on both cut lines of a 2x2 split: 4 steps reach relres <=
+    1e-3, the converged field deviates <= 1e-6 from the reference's global
+    direct solve (tests/golden/a2_direct.npz, make_golden_a2.py); the reference
+    converges in 4 steps."""
+    import os
+    import sys
+    import numpy as np
+    from conftest import rel_l2
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden"))
+    from make_golden_a2 import problem
+    prob = problem()
+    ud = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                              "a2_direct.npz"))["u"].astype(np.complex128)
+    with DdmEngine(prob) as e:
+        f = prob.source_f()
+        st4 = DdmStats()
+        e.solve_iterative(f, 0.0, 4, st4)
+        assert st4.relres <= 1e-3
+        st = DdmStats()
+        u = e.solve_iterative(f, 1e-8, 60, st)
+    assert st.converged and st.steps == 4
+    assert rel_l2(u, ud) <= 1e-6
