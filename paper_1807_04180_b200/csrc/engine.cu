@@ -218,7 +218,9 @@ struct hddm_engine {
   StepArgs step_args(int s, const cplx* f);
   // solve of the RHS t with (flag[t] != 0) == on: B -> X (Y scratch)
   SolveArgs solve_args(const cplx* B, cplx* X, cplx* Y, const int* flag, int on);
-  void enqueue_solve(const SolveArgs& A, cudaStream_t stream);
+  // the batched solve; with `check`, each tile group's residual partials are
+  // queued right behind its solve (overlapping the other groups' chains)
+  void enqueue_solve(const SolveArgs& A, cudaStream_t stream, const CheckArgs* check = nullptr);
   int* d_zero = nullptr;  // nsub zero flags: every RHS active
   long long fwd_entries_full = 0, fwd_entries_sparse = 0;  // factor entries per forward sweep
   VMap vmap() const {
@@ -1196,21 +1198,25 @@ void hddm_engine::enqueue_step_front(int s, cudaStream_t stream, unsigned long l
     CK(cudaMemsetAsync(A.Ucur, 0, size_t(nsub) * nw * sizeof(cplx), stream));
     SA.sparse_rhs = 1;
   }
-  if (!no_solve) enqueue_solve(SA, stream);
-  if (no_solve)
-    launch_check(check_args(d_B, A.Ucur, A.zc, nullptr), stream);
-  else
-    launch_check_init(check_args(d_B, A.Ucur, A.zc, nullptr), refine_args(d_B, A.Ucur, A.zc, cond),
-                      d_done, stream);
+  const CheckArgs C = check_args(d_B, A.Ucur, A.zc, nullptr);
+  if (no_solve) {
+    launch_check(C, stream);
+  } else {
+    // each group's check runs behind its own solve; the statistics after the join
+    enqueue_solve(SA, stream, &C);
+    launch_finish_init(C, refine_args(d_B, A.Ucur, A.zc, cond), d_done, stream);
+  }
 }
 
 // The batched solve on `stream`. On the engine stream, every class runs its
 // level chain on its own forked stream (classes overlap; a class's vectors stay
 // L2-resident between its consecutive levels), joined afterwards.
-void hddm_engine::enqueue_solve(const SolveArgs& SA, cudaStream_t stream) {
+void hddm_engine::enqueue_solve(const SolveArgs& SA, cudaStream_t stream, const CheckArgs* check) {
   const int nt = int(plan.groups.size());
   if (!per_class_streams || nt == 1 || (stream != st && stream != st2)) {
     for (int g = 0; g < nt; ++g) launch_solve_group(SA, plan, g, stream);
+    if (check)
+      for (int g = 0; g < nt; ++g) launch_check_tiles(*check, plan.groups[g], stream);
     return;
   }
   // one stream set per origin stream: st (step front) and st2 (the refinement
@@ -1229,6 +1235,7 @@ void hddm_engine::enqueue_solve(const SolveArgs& SA, cudaStream_t stream) {
   for (int g = 0; g < nt; ++g) {
     CK(cudaStreamWaitEvent(F.st[g], F.fork, 0));
     launch_solve_group(SA, plan, g, F.st[g]);
+    if (check) launch_check_tiles(*check, plan.groups[g], F.st[g]);
     CK(cudaEventRecord(F.ev[g], F.st[g]));
   }
   for (int g = 0; g < nt; ++g) CK(cudaStreamWaitEvent(stream, F.ev[g], 0));

@@ -198,6 +198,10 @@ struct RefineArgs;
 // check partials, then per-RHS rel + refinement init (refine's first pass) in one kernel;
 // `done` is a zeroed device counter
 void launch_check_init(const CheckArgs& A, const RefineArgs& R, int* done, cudaStream_t st);
+// the check of one tile group's members (queued on the group's stream after its
+// solve) and, after all groups, the per-RHS statistics + refinement init
+void launch_check_tiles(const CheckArgs& A, const TileArg& G, cudaStream_t st);
+void launch_finish_init(const CheckArgs& A, const RefineArgs& R, int* done, cudaStream_t st);
 
 // Iterative refinement on device (refine, proj/src/sparse.cpp:268-292): per RHS
 // state after the first solve; corrections run inside a conditional WHILE graph

@@ -281,13 +281,18 @@ __device__ __forceinline__ cplx ax_row_t(XV X, int pos, int wnx, int wny, double
   return ax;
 }
 
-__global__ void __launch_bounds__(256, HDDM_CHECK_MINB) k_check(CheckArgs A) {
-  __shared__ double sr[256], sb[256];
-  const int c = blockIdx.y;
+// Residual partials of members [k0, k0 + M) of class c over position chunk
+// blockIdx.x: thread t serves member k0 + t % M at positions t / M,
+// t / M + 256 / M, ... of the chunk (a warp reads consecutive members:
+// contiguous addresses). Members of a class have bitwise-identical window
+// operators (the class criterion), so the coefficients come from the class
+// representative. Per-member sums combine in fixed thread order.
+__device__ __forceinline__ void check_block(const CheckArgs& A, int c, int k0, int M, double* sr,
+                                            double* sb) {
   const int c0 = A.vm.cptr[c], m = A.vm.cptr[c + 1] - c0;
   const int tid = threadIdx.x;
-  const int per = 256 / m;  // positions per sweep of the block (m <= 256)
-  const int k = tid % m, pi = tid / m;
+  const int per = 256 / M;  // positions per sweep of the block (M <= 256)
+  const int k = k0 + tid % M, pi = tid / M;
   const int t = A.vm.cmem[c0 + k];
   const bool act = pi < per && (A.only ? A.only[t] != 0 : !A.zc[t]);
   double r2 = 0, b2 = 0;
@@ -311,16 +316,45 @@ __global__ void __launch_bounds__(256, HDDM_CHECK_MINB) k_check(CheckArgs A) {
   sr[tid] = r2;
   sb[tid] = b2;
   __syncthreads();
-  if (tid < m) {
+  if (tid < M) {
     double R = 0, Bs = 0;
-    for (int q = tid; q < per * m; q += m) {
+    for (int q = tid; q < per * M; q += M) {
       R += sr[q];
       Bs += sb[q];
     }
-    const int tk = A.vm.cmem[c0 + tid];
+    const int tk = A.vm.cmem[c0 + k0 + tid];
     A.part[((long long)tk * A.nchunk + blockIdx.x) * 2 + 0] = R;
     A.part[((long long)tk * A.nchunk + blockIdx.x) * 2 + 1] = Bs;
   }
+}
+
+__global__ void k_finish_init(CheckArgs A, RefineArgs R, int* done);
+
+// all members of class blockIdx.y
+__global__ void __launch_bounds__(256, HDDM_CHECK_MINB) k_check(CheckArgs A) {
+  __shared__ double sr[256], sb[256];
+  const int c = blockIdx.y;
+  check_block(A, c, 0, A.vm.cptr[c + 1] - A.vm.cptr[c], sr, sb);
+}
+
+// the members of tile blockIdx.y of a tile group (right after that group's solve)
+__global__ void __launch_bounds__(256, HDDM_CHECK_MINB) k_check_tiles(CheckArgs A, TileArg G) {
+  __shared__ double sr[256], sb[256];
+  const TileRec* r = G.rec + blockIdx.y;
+  const int c = r->c;
+  check_block(A, c, int(r->cb - A.vm.cbase[c]), G.M, sr, sb);
+}
+
+void launch_check_tiles(const CheckArgs& A, const TileArg& G, cudaStream_t st) {
+  if (G.ntile == 0) return;
+  k_check_tiles<<<dim3(A.nchunk, G.ntile), 256, 0, st>>>(A, G);
+}
+
+// per-RHS rel + refinement init from partials already written (after the
+// per-group checks of the forked solve)
+void launch_finish_init(const CheckArgs& A, const RefineArgs& R, int* done, cudaStream_t st) {
+  cudaMemsetAsync(R.any, 0, sizeof(int), st);
+  k_finish_init<<<unsigned((A.nsub * 32 + 255) / 256), 256, 0, st>>>(A, R, done);
 }
 
 __global__ void k_check_finish(CheckArgs A, int nsub) {
@@ -347,7 +381,7 @@ __device__ __forceinline__ void set_cond(unsigned long long h, int v) {
 // check_finish + refine_init in one pass: a warp per right-hand side sums its
 // partials (fixed tree order), records rel for the stopping statistics and the
 // refinement state; the last block to finish sets the WHILE condition.
-__global__ void __launch_bounds__(256) k_finish_init(CheckArgs A, RefineArgs R, int* done) {
+__global__ void k_finish_init(CheckArgs A, RefineArgs R, int* done) {
   const int lane = threadIdx.x & 31;
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int need = 0;
