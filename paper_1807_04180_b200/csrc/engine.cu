@@ -835,6 +835,7 @@ void hddm_engine::build_plan() {
       plan.fwd_sp.push_back(F);
     }
     plan.d_fseg_sp = upload(fseg_sp);
+    plan.d_sn_live = upload(std::vector<unsigned char>(act.begin(), act.end()));
     plan.has_sparse = true;
     fwd_entries_full = 0;
     fwd_entries_sparse = 0;
@@ -994,6 +995,7 @@ SolveArgs hddm_engine::solve_args(const cplx* Bp, cplx* X, cplx* Yp, const int* 
   A.flag = flag;
   A.flag_on = on;
   A.sparse_rhs = 0;
+  A.sn_live = nullptr;
   A.B = Bp;
   A.X = X;
   A.Y = Yp;
@@ -1195,7 +1197,10 @@ void hddm_engine::enqueue_step_front(int s, cudaStream_t stream, unsigned long l
   static const bool no_solve = std::getenv("HDDM_STEP_NOSOLVE") != nullptr;  // profiling aid
   SolveArgs SA = solve_args(d_B, A.Ucur, d_Y, A.zc, 0);
   if (s >= 2 && plan.has_sparse) {  // RHS nonzero only on the transfer patches
-    CK(cudaMemsetAsync(A.Ucur, 0, size_t(nsub) * nw * sizeof(cplx), stream));
+    // skipped subtrees read as z = 0 in the backward (zval), so X need not be
+    // cleared (HDDM_CLEAR_X: clear it anyway, A/B timing aid)
+    static const bool clear_x = std::getenv("HDDM_CLEAR_X") != nullptr;
+    if (clear_x) CK(cudaMemsetAsync(A.Ucur, 0, size_t(nsub) * nw * sizeof(cplx), stream));
     SA.sparse_rhs = 1;
   }
   const CheckArgs C = check_args(d_B, A.Ucur, A.zc, nullptr);
@@ -1834,23 +1839,42 @@ int hddm_time_solve(hddm_engine* e, int reps, double* ms_per_solve) {
     e->enqueue_solve(e->solve_args(e->d_B, e->d_C, e->d_Y, e->d_zero, on), st);
     set_solve_skip(0, -1);
     CK(cudaStreamEndCapture(st, &g));
-    cudaGraphExec_t x;
+    cudaGraphExec_t x, x2 = nullptr;
     CK(cudaGraphInstantiate(&x, g, 0));
+    // HDDM_TIME_PAIR (profiling aid, results invalid): two instances run
+    // concurrently on two streams; the time per solve then shows how much idle
+    // capacity the single solve graph leaves
+    const bool pair = std::getenv("HDDM_TIME_PAIR") != nullptr;
+    if (pair) CK(cudaGraphInstantiate(&x2, g, 0));
     CK(cudaGraphDestroy(g));
     CK(cudaGraphLaunch(x, st));  // warm-up
-    cudaEvent_t a, b;
+    cudaEvent_t a, b, j;
     CK(cudaEventCreate(&a));
     CK(cudaEventCreate(&b));
+    CK(cudaEventCreate(&j));
     CK(cudaEventRecord(a, st));
-    for (int r = 0; r < reps; ++r) CK(cudaGraphLaunch(x, st));
+    for (int r = 0; r < reps; ++r) {
+      if (pair) {
+        CK(cudaEventRecord(j, st));
+        CK(cudaStreamWaitEvent(e->st2, j, 0));
+        CK(cudaGraphLaunch(x2, e->st2));
+      }
+      CK(cudaGraphLaunch(x, st));
+      if (pair) {
+        CK(cudaEventRecord(j, e->st2));
+        CK(cudaStreamWaitEvent(st, j, 0));
+      }
+    }
     CK(cudaEventRecord(b, st));
     CK(cudaEventSynchronize(b));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, a, b));
-    *ms_per_solve = ms / std::max(reps, 1);
+    *ms_per_solve = ms / std::max(reps, 1) / (pair ? 2 : 1);
     cudaEventDestroy(a);
     cudaEventDestroy(b);
+    cudaEventDestroy(j);
     cudaGraphExecDestroy(x);
+    if (x2) cudaGraphExecDestroy(x2);
   });
 }
 

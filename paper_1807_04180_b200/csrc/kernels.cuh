@@ -26,6 +26,9 @@ struct SolveArgs {
   const int* flag;     // per RHS t: active iff (flag[t] != 0) == flag_on
   int flag_on;
   int sparse_rhs;      // host: RHS nonzero only on the transfer patches (forward plan fwd_sp)
+  // sparse RHS only (else null): supernodes the forward touched; the others hold
+  // z = 0 exactly, which the backward reads as 0 (X is not cleared)
+  const unsigned char* sn_live;
   const cplx* B;       // right-hand sides (factor order), layout vm
   cplx* X;             // solutions (factor order), layout vm
   cplx* Y;             // scratch, layout vm
@@ -76,6 +79,7 @@ struct SolvePlan {
   bool has_sparse = false;
   SegRec* d_fseg = nullptr;            // segments referenced by fwd levels' records
   SegRec* d_fseg_sp = nullptr;         // live segments (active sources) for fwd_sp
+  unsigned char* d_sn_live = nullptr;  // per supernode: in a subtree holding a patch node
   std::vector<SolveLevel> bwd;         // separator columns by depth (pull, then diag)
   SolveLevel bwd_leafcol;              // leaf columns: w = Dinv z - B^T x
   SolveLevel bwd_leaf;                 // leaves: band back-substitution

@@ -141,6 +141,12 @@ __device__ __forceinline__ cplx seg_dot(const cplx* __restrict__ vals, const Seg
   return cadd(acc0, acc1);
 }
 
+// forward result z at position p of supernode s: supernodes the sparse-RHS
+// forward skipped hold z = 0 exactly and X is not cleared for them
+__device__ __forceinline__ cplx zval(const SolveArgs& A, int s, long long p) {
+  return (A.sn_live != nullptr && A.sn_live[s] == 0) ? cmk(0, 0) : A.X[p];
+}
+
 // rows of a backward list (sorted by first stored column) that touch column j
 __device__ __forceinline__ int rows_upto(const BwRow* rows, int nr, int j) {
   int lo = 0, hi = nr;  // first index with first > j
@@ -332,7 +338,7 @@ __global__ void __launch_bounds__(kThreads) k_bwd_pull(SolveArgs A, TileArg T, c
   const int nr = rows_upto(rows, A.bw_ptr[item.x + 1] - A.bw_ptr[item.x], j);
   const cplx acc = bw_gather<kUB>(vals, rows, 0, nr, 1, j, A.X + L.cb, L.m);
   const long long p = vat(L, sn.c0 + j);
-  (TO_X ? A.X : A.Y)[p] = csub(cmul(ldg(vals + sn.dinv_off + j), A.X[p]), acc);
+  (TO_X ? A.X : A.Y)[p] = csub(cmul(ldg(vals + sn.dinv_off + j), zval(A, item.x, p)), acc);
 }
 
 // separator columns, backward diagonal: X[j] = Y[j] + sum_{i>j} Linv[i][j] Y[i]
@@ -413,7 +419,7 @@ __global__ void __launch_bounds__(kSplitWarps * 32) k_bwd_split(SolveArgs A, Til
     if (DIAG)
       A.X[p] = cadd(A.Y[p], sum);
     else
-      A.Y[p] = csub(cmul(ldg(vals + sn.dinv_off + j), A.X[p]), sum);
+      A.Y[p] = csub(cmul(ldg(vals + sn.dinv_off + j), zval(A, item.x, p)), sum);
   }
 }
 
@@ -526,7 +532,7 @@ __global__ void __launch_bounds__(kStageThreads) k_bwd_stage(SolveArgs A, TileAr
       if ((A.flag[rec->t[mm]] != 0) == (A.flag_on != 0)) {
         const int j = j0 + jj;
         const long long a = cb + (long long)(sn.c0 + j) * m + mm;
-        (TO_X ? A.X : A.Y)[a] = csub(cmul(ldg(vals + sn.dinv_off + j), A.X[a]), acc[q]);
+        (TO_X ? A.X : A.Y)[a] = csub(cmul(ldg(vals + sn.dinv_off + j), zval(A, ch.x, a)), acc[q]);
       }
     }
   }
@@ -665,11 +671,12 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
   const TileArg T1 = with_shape(P.groups[g], 1);  // thread per (item, member)
   const long long nt = T1.ntile;
   auto blocks = [nt](long long items, int R) { return blocks_for(nt * ((items + R - 1) / R) * 32); };
-  // sparse RHS (steps >= 2): X was cleared; ring rows and patch-free subtrees stay 0
+  // sparse RHS (steps >= 2): patch-free subtrees are skipped (z = 0, see zval)
   const bool sp = A0.sparse_rhs && P.has_sparse;
   SolveArgs A = A0;
   A.fseg = sp ? P.d_fseg_sp : P.d_fseg;
-  if (!(skip & 1) && !sp) k_ring<<<blocks(A.nring, T1.R), kThreads, 0, st>>>(A, T1);
+  A.sn_live = sp ? P.d_sn_live : nullptr;
+  if (!(skip & 1)) k_ring<<<blocks(A.nring, T1.R), kThreads, 0, st>>>(A, T1);
   const SolveLevel& FL = sp ? P.fwd_leaf_sp : P.fwd_leaf;
   if (!(skip & 2) && FL.nitem > 0)
     launch_pdl(k_fwd_leaf, blocks(FL.nitem, T1.R), kThreads, 0, st, A, T1, (const int2*)FL.d_items,
