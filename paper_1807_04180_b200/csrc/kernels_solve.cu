@@ -121,18 +121,33 @@ template <int U>
 __device__ __forceinline__ cplx seg_dot(const cplx* __restrict__ vals, const SegRec* __restrict__ sg,
                                         int ns, int e, int E, const cplx* __restrict__ X, int m) {
   cplx acc0 = cmk(0, 0), acc1 = cmk(0, 0);
+  const long long xs = (long long)E * m;  // vector stride per step: pointer increments only
   for (int k = 0; k < ns; ++k) {
     const SegRec r = sg[k];
-    const cplx* L = vals + r.off;
-    const cplx* Xs = X + (long long)r.zb * m;
-    for (int q0 = e; q0 < r.len; q0 += U * E) {
+    if (e >= r.len) continue;
+    int n = (r.len - 1 - e) / E + 1;  // entries of this lane
+    const cplx* lp = vals + r.off + e;
+    const cplx* xp = X + (long long)(r.zb + e) * m;
+    for (; n >= U; n -= U) {  // full batches of U
       cplx l[U], x[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int q = q0 + u * E;
-        const bool ok = q < r.len;
-        l[u] = ok ? ldf(L + q) : cmk(0, 0);
-        x[u] = ok ? Xs[(long long)q * m] : cmk(0, 0);
+        l[u] = ldf(lp);
+        x[u] = *xp;
+        lp += E;
+        xp += xs;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) cfma((u & 1) ? acc1 : acc0, l[u], x[u]);
+    }
+    if (n > 0) {  // tail: one predicated batch
+      cplx l[U], x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        l[u] = u < n ? ldf(lp) : cmk(0, 0);
+        x[u] = u < n ? *xp : cmk(0, 0);
+        lp += E;
+        xp += xs;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) cfma((u & 1) ? acc1 : acc0, l[u], x[u]);
@@ -299,16 +314,21 @@ __global__ void __launch_bounds__(kThreads) k_fwd_diag(SolveArgs A, TileArg T, c
     const DevSn sn = A.sn[item.x];
     const int i = item.y;
     y0 = vat(L, sn.c0);
-    const SVec<const cplx> y{A.Y + y0, L.m};
     const cplx* row = A.vals + (long long)L.c * A.nvals + sn.diag_off + (long long)i * (i - 1) / 2;
+    const int E = T.E;
+    const long long ys = (long long)E * L.m;
+    const cplx* lp = row + L.e;
+    const cplx* yp = A.Y + y0 + (long long)L.e * L.m;
     int j = L.e;
-    for (; j + T.E < i; j += 2 * T.E) {
-      const cplx l0 = ldf(row + j), l1 = ldf(row + j + T.E);
-      const cplx v0 = y[j], v1 = y[j + T.E];
+    for (; j + E < i; j += 2 * E) {
+      const cplx l0 = ldf(lp), l1 = ldf(lp + E);
+      const cplx v0 = *yp, v1 = yp[ys];
       cfma(acc, l0, v0);
       cfma(acc2, l1, v1);
+      lp += 2 * E;
+      yp += 2 * ys;
     }
-    if (j < i) cfma(acc, ldf(row + j), y[j]);
+    if (j < i) cfma(acc, ldf(lp), *yp);
   }
   acc = cadd(acc, acc2);
   if (T.E > 1) acc = tile_reduce(acc, T, L);
@@ -353,22 +373,32 @@ __global__ void __launch_bounds__(kThreads) k_bwd_diag(SolveArgs A, TileArg T, c
   const int2 item = items[it];
   const DevSn sn = A.sn[item.x];
   const int j = item.y;
-  const cplx* Linv = A.vals + (long long)L.c * A.nvals + sn.diag_off;
-  const SVec<const cplx> y{A.Y + vat(L, sn.c0), L.m};
-  cplx acc = y[j], acc2 = cmk(0, 0);
+  const int m = L.m;
+  const cplx* yp = A.Y + vat(L, sn.c0 + j);
+  cplx acc = *yp, acc2 = cmk(0, 0);
   int i = j + 1;
+  // column j of the packed strictly-lower inverse (row i starts at i(i-1)/2):
+  // rows i+1, i+2, i+3, i+4 are i, 2i+1, 3i+3, 4i+6 entries further
+  const cplx* lp = A.vals + (long long)L.c * A.nvals + sn.diag_off + (long long)i * (i - 1) / 2 + j;
+  yp += m;
   for (; i + 4 <= sn.n; i += 4) {
-    const cplx l0 = ldf(Linv + (long long)i * (i - 1) / 2 + j);
-    const cplx l1 = ldf(Linv + (long long)(i + 1) * i / 2 + j);
-    const cplx l2 = ldf(Linv + (long long)(i + 2) * (i + 1) / 2 + j);
-    const cplx l3 = ldf(Linv + (long long)(i + 3) * (i + 2) / 2 + j);
-    const cplx y0 = y[i], y1 = y[i + 1], y2 = y[i + 2], y3 = y[i + 3];
+    const cplx l0 = ldf(lp);
+    const cplx l1 = ldf(lp + i);
+    const cplx l2 = ldf(lp + 2 * i + 1);
+    const cplx l3 = ldf(lp + 3 * i + 3);
+    const cplx y0 = yp[0], y1 = yp[m], y2 = yp[2 * m], y3 = yp[3 * m];
     cfma(acc, l0, y0);
     cfma(acc2, l1, y1);
     cfma(acc, l2, y2);
     cfma(acc2, l3, y3);
+    lp += 4 * i + 6;
+    yp += 4 * m;
   }
-  for (; i < sn.n; ++i) cfma(acc, ldf(Linv + (long long)i * (i - 1) / 2 + j), y[i]);
+  for (; i < sn.n; ++i) {
+    cfma(acc, ldf(lp), *yp);
+    lp += i;
+    yp += m;
+  }
   A.X[vat(L, sn.c0 + j)] = cadd(acc, acc2);
 }
 
@@ -473,21 +503,25 @@ __global__ void __launch_bounds__(kStageThreads) k_bwd_stage(SolveArgs A, TileAr
 #pragma unroll
   for (int q = 0; q < kMaxQ; ++q) acc[q] = cmk(0, 0);
   pdl_wait();
+  // staging lanes on (row, member) and (row, column) grids: no divisions in the loops
+  const int xr = tid / M, xm = tid - xr * M, xrows = kStageThreads / M;
+  const int lr = tid / CW, lc = tid - lr * CW, lrows = kStageThreads / CW;
+  const cplx* Xb = A.X + cb + xm;
   for (int k0 = 0; k0 < nre; k0 += RC) {
     const int kc = min(RC, nre - k0);
     for (int kk = tid; kk < kc; kk += kStageThreads) rd[kk] = rows[k0 + kk];
     __syncthreads();
-    for (int e = tid; e < kc * M; e += kStageThreads) {
-      const int kk = e / M, mm = e - kk * M;
-      cp_async16(xs + e, A.X + cb + (long long)rd[kk].dpos * m + mm);
-    }
-    for (int e = tid; e < kc * CW; e += kStageThreads) {
-      const int kk = e / CW, j = j0 + (e - kk * CW);
-      const BwRow d = rd[kk];
-      if (j >= d.first)
-        cp_async16(ls + e, vals + d.off + (j - d.first));
-      else
-        ls[e] = cmk(0, 0);
+    if (xr < xrows)
+      for (int kk = xr; kk < kc; kk += xrows) cp_async16(xs + kk * M + xm, Xb + (long long)rd[kk].dpos * m);
+    if (lr < lrows) {
+      const int j = j0 + lc;
+      for (int kk = lr; kk < kc; kk += lrows) {
+        const BwRow d = rd[kk];
+        if (j >= d.first)
+          cp_async16(ls + kk * CW + lc, vals + d.off + (j - d.first));
+        else
+          ls[kk * CW + lc] = cmk(0, 0);
+      }
     }
     cp_async_wait_all();
     __syncthreads();
