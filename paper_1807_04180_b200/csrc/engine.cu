@@ -1832,7 +1832,10 @@ int hddm_time_solve(hddm_engine* e, int reps, double* ms_per_solve) {
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     set_solve_skip(std::getenv("HDDM_SKIP") ? std::atoi(std::getenv("HDDM_SKIP")) : 0,
-                   std::getenv("HDDM_ONLY_TILE") ? std::atoi(std::getenv("HDDM_ONLY_TILE")) : -1);
+                   std::getenv("HDDM_ONLY_TILE")
+                       ? std::atoi(std::getenv("HDDM_ONLY_TILE"))
+                       : (std::getenv("HDDM_ONLY_M") ? -2 - std::atoi(std::getenv("HDDM_ONLY_M")) : -1));
+    // HDDM_ONLY_M=M: only the tile groups of M members (profiling aid)
     // HDDM_TIME_EMPTY: no RHS active -- every kernel exits after its setup, so
     // the time is the launch / dependency floor of the solve graph (profiling aid)
     const int on = std::getenv("HDDM_TIME_EMPTY") ? 1 : 0;

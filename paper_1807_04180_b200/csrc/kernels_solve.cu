@@ -702,6 +702,7 @@ static void launch_bwd_stage(const SolveArgs& A, const TileArg& T, const SolveLe
 void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStream_t st) {
   const int skip = skip_mask();
   if (g_only >= 0 && g != g_only) return;
+  if (g_only <= -2 && P.groups[g].M != -2 - g_only) return;  // HDDM_ONLY_M (time_solve only)
   const TileArg T1 = with_shape(P.groups[g], 1);  // thread per (item, member)
   const long long nt = T1.ntile;
   auto blocks = [nt](long long items, int R) { return blocks_for(nt * ((items + R - 1) / R) * 32); };
