@@ -672,14 +672,20 @@ void hddm_engine::build_plan() {
     std::map<int, std::vector<TileRec>> byM;
     for (int c = 0; c < ncls; ++c) {
       const int m = S.cls_ptr[c + 1] - S.cls_ptr[c];
-      for (int k0 = 0; k0 < m; k0 += 32) {
+      // ceil(m / tile_max) tiles of near-equal size: a 36-member class (config 2) runs as
+      // 12 + 12 + 12 (0.935 -> 0.834 ms per solve), not 32 + 4; config 4 keeps its 14s
+      static const int tile_max =
+          std::max(1, std::min(32, std::getenv("HDDM_TILE_MAX") ? std::atoi(std::getenv("HDDM_TILE_MAX")) : 16));
+      const int nt = (m + tile_max - 1) / tile_max;
+      for (int ti = 0, k0 = 0; ti < nt; ++ti) {
+        const int M = m / nt + (ti < m % nt ? 1 : 0);
         TileRec T = {};
         T.cb = (long long)S.cls_ptr[c] * nw + k0;
         T.c = c;
         T.m = m;
-        const int M = std::min(32, m - k0);
         for (int k = 0; k < 32; ++k) T.t[k] = S.cls_members[S.cls_ptr[c] + k0 + std::min(k, M - 1)];
         byM[M].push_back(T);
+        k0 += M;
       }
     }
     // 4 tiles per group measured best at config 4 (more, shorter launch chains
