@@ -303,6 +303,12 @@ def run_ours(args, world, rank, local):
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
                    "sample": f"{type(exc).__name__}: {exc}"}
 
+    fp = eng.footprint()
+    factor_info = {"ms": eng.factor_ms(), "classes": len(ci),
+                   "stored_values_per_class": fp["stored_values_per_class"],
+                   "factor_bytes": 16 * fp["stored_values_per_class"] * len(ci),
+                   "device_bytes_in_use": fp["device_bytes_in_use"],
+                   "hbm_bytes": 180e9}
     fac_b = 16.0 * sum(nnz)
     vec_b = 16.0 * 6 * prob.nsub * prob.window[0] * prob.window[1]
     l2_note = (f"factors {fac_b / 1e6:.0f} MB + per-subdomain vectors {vec_b / 1e6:.0f} MB vs "
@@ -333,6 +339,7 @@ def run_ours(args, world, rank, local):
                               "bytes_per_step_full": B["B_step"],
                               "fwd_entries": {"full": fwd_full, "sparse_rhs": fwd_sparse},
                               "frac": step_achieved / peak, "all_active": all_active},
+            "factor": factor_info,
             "solve_launches_per_step": eng.solve_launches(),
             "refine": {"max_first_pass_relres": max_local_rel,
                        "solves_corrected": corrections},
