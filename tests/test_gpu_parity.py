@@ -139,12 +139,17 @@ def test_lens_medium_matches_oracle():
     e.close()
 
 
-def test_cfg2_fgmres_matches_oracle():
-    """BASELINE config 2 end to end (1024^2, 8x8, FGMRES(30)+DDM(K=16)) against
-    the C restatement (pinned bit-for-bit to the reference by test_oracle)."""
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_fullsize_fgmres_matches_oracle(cfg):
+    """BASELINE configs 2 and 3 end to end at full size (1024^2, 8x8,
+    FGMRES(30)+DDM(K=16); config 3 is the lens medium, 64 distinct windows)
+    against the C restatement (pinned bit-for-bit to the reference by
+    test_oracle; for the lens medium, which the reference lacks, the same
+    formulas with the clamped lens k^2): identical iteration count and solve /
+    skip counts, final x <= 1e-8, the first preconditioner application <= 1e-10."""
     from paper_1807_04180_b200.engine import DdmEngine, DdmStats, FgmresOptions
     from paper_1807_04180_b200.problems import config
-    prob = config(2)
+    prob = config(cfg)
     e = DdmEngine(prob)
     o = pyoracle.OracleEngine(prob)
     f = prob.source_f()
