@@ -1198,8 +1198,10 @@ RefineArgs hddm_engine::refine_args(const cplx* Bp, cplx* X, const int* zc,
 // refine pass: flags -> RHS assembly -> batched solves -> residual check.
 void hddm_engine::enqueue_step_front(int s, cudaStream_t stream, unsigned long long cond) {
   const StepArgs A = step_args(s, d_f);
-  launch_flags(A, ncls, stream);
-  launch_gather(A, stream);
+  // HDDM_STEP_SKIP (profiling aid, results invalid): 1 flags, 2 gather, 4 check, 8 accumulate
+  static const int sskip = std::getenv("HDDM_STEP_SKIP") ? std::atoi(std::getenv("HDDM_STEP_SKIP")) : 0;
+  if (!(sskip & 1)) launch_flags(A, ncls, stream);
+  if (!(sskip & 2)) launch_gather(A, stream);
   static const bool no_solve = std::getenv("HDDM_STEP_NOSOLVE") != nullptr;  // profiling aid
   SolveArgs SA = solve_args(d_B, A.Ucur, d_Y, A.zc, 0);
   if (s >= 2 && plan.has_sparse) {  // RHS nonzero only on the transfer patches
@@ -1211,7 +1213,9 @@ void hddm_engine::enqueue_step_front(int s, cudaStream_t stream, unsigned long l
   }
   const CheckArgs C = check_args(d_B, A.Ucur, A.zc, nullptr);
   if (no_solve) {
-    launch_check(C, stream);
+    if (!(sskip & 4)) launch_check(C, stream);
+  } else if (sskip & 4) {
+    enqueue_solve(SA, stream, nullptr);
   } else {
     // each group's check runs behind its own solve; the statistics after the join
     enqueue_solve(SA, stream, &C);
@@ -1294,7 +1298,8 @@ void hddm_engine::build_step_graph(int v) {
   enqueue_refine_body(s, st2, (unsigned long long)h);
   cudaGraph_t bout;
   CK(cudaStreamEndCapture(st2, &bout));
-  launch_accumulate(step_args(s, d_f), st);
+  static const int sskip = std::getenv("HDDM_STEP_SKIP") ? std::atoi(std::getenv("HDDM_STEP_SKIP")) : 0;
+  if (!(sskip & 8)) launch_accumulate(step_args(s, d_f), st);
   cudaGraph_t gout;
   CK(cudaStreamEndCapture(st, &gout));
   CK(cudaGraphInstantiate(&step_exec[v], g, 0));
@@ -1845,7 +1850,11 @@ int hddm_time_solve(hddm_engine* e, int reps, double* ms_per_solve) {
     // HDDM_TIME_EMPTY: no RHS active -- every kernel exits after its setup, so
     // the time is the launch / dependency floor of the solve graph (profiling aid)
     const int on = std::getenv("HDDM_TIME_EMPTY") ? 1 : 0;
-    e->enqueue_solve(e->solve_args(e->d_B, e->d_C, e->d_Y, e->d_zero, on), st);
+    SolveArgs SA = e->solve_args(e->d_B, e->d_C, e->d_Y, e->d_zero, on);
+    // HDDM_TIME_SPARSE: the steady-state (steps >= 2) forward plan; B then holds the last
+    // step's right-hand sides, which are nonzero only on the transfer patches
+    if (std::getenv("HDDM_TIME_SPARSE") && e->plan.has_sparse) SA.sparse_rhs = 1;
+    e->enqueue_solve(SA, st);
     set_solve_skip(0, -1);
     CK(cudaStreamEndCapture(st, &g));
     cudaGraphExec_t x, x2 = nullptr;

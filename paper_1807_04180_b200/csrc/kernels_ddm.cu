@@ -304,12 +304,32 @@ __device__ __forceinline__ void check_block(const CheckArgs& A, int c, int k0, i
     const SVec<const cplx> Bv{A.B + A.vm.cbase[c] + k, m};
     const int chunk = (A.nw + A.nchunk - 1) / A.nchunk;
     const int p0 = blockIdx.x * chunk, p1 = min(A.nw, p0 + chunk);
+    // the next position's structural tables are loaded one iteration ahead, so
+    // the vector / coefficient loads of a position (which depend on them) are
+    // the only round trip per iteration
+    int pos = p0 + pi;
+    int2 lq_n = make_int2(-1, 0);
+    int4 nb_n = make_int4(-1, -1, -1, -1);
+    double k2_n = 0;
+    if (pos < p1) {
+      lq_n = __ldg(A.lpq + pos);
+      nb_n = __ldg(A.nbr + pos);
+      k2_n = __ldg(k2c + pos);
+    }
 #pragma unroll kCheckUnroll
-    for (int pos = p0 + pi; pos < p1; pos += per) {
+    for (; pos < p1; pos += per) {
+      const int2 lq = lq_n;
+      const int4 nb = nb_n;
+      const double k2 = k2_n;
+      const int pn = pos + per;
+      if (pn < p1) {
+        lq_n = __ldg(A.lpq + pn);
+        nb_n = __ldg(A.nbr + pn);
+        k2_n = __ldg(k2c + pn);
+      }
       const cplx b = Bv[pos];
       b2 += cnorm2(b);
-      const cplx ax = ax_row_t(X, pos, A.wnx, A.wny, A.ih2, sa, __ldg(k2c + pos), __ldg(A.lpq + pos),
-                               __ldg(A.nbr + pos));
+      const cplx ax = ax_row_t(X, pos, A.wnx, A.wny, A.ih2, sa, k2, lq, nb);
       r2 += cnorm2(csub(b, ax));
     }
   }
