@@ -150,6 +150,7 @@ struct hddm_engine {
   cplx* d_asm = nullptr;
   cplx* d_tmp = nullptr;
   int* d_colcov = nullptr;
+  unsigned char* d_bmask = nullptr;  // per factor position: in the transfer-patch union
   int* d_pnode = nullptr;
   int* d_pmask = nullptr;
   int* d_xfer_pos = nullptr;
@@ -243,7 +244,7 @@ struct hddm_engine {
     CK(cudaMemcpy2DAsync(h, sizeof(cplx), dv + h_vbase[t], sizeof(cplx) * h_vstr[t], sizeof(cplx), nw,
                          cudaMemcpyDeviceToHost, s));
   }
-  CheckArgs check_args(const cplx* Bp, const cplx* X, const int* zc, const int* only);
+  CheckArgs check_args(const cplx* Bp, const cplx* X, const int* zc, const int* only, bool sparse_b = false);
   RefineArgs refine_args(const cplx* Bp, cplx* X, const int* zc, unsigned long long cond);
   void enqueue_step_front(int s, cudaStream_t stream, unsigned long long cond);
   void enqueue_refine_body(int s, cudaStream_t stream, unsigned long long cond);
@@ -563,6 +564,9 @@ void hddm_engine::create(const hddm_problem& p) {
     }
     npatch = int(pn.size());
     d_pnode = upload(pn);
+    std::vector<unsigned char> bm(nw, 0);
+    for (int k = 0; k < nw; ++k) bm[k] = mask[Y.perm[k]] ? 1 : 0;
+    d_bmask = upload(bm);
     d_pmask = upload(pm);
     // per (patch node, direction, stencil point C E W N S): the source-window
     // position and transfer_beta (partition.cpp:131-152) -- window-local, so
@@ -1122,8 +1126,9 @@ void hddm_engine::reset_state() {
 }
 
 CheckArgs hddm_engine::check_args(const cplx* Bp, const cplx* X, const int* zc,
-                                  const int* only) {
+                                  const int* only, bool sparse_b) {
   CheckArgs C;
+  C.bmask = sparse_b ? d_bmask : nullptr;
   C.nw = nw;
   C.wnx = wnx;
   C.wny = wny;
@@ -1211,7 +1216,9 @@ void hddm_engine::enqueue_step_front(int s, cudaStream_t stream, unsigned long l
     if (clear_x) CK(cudaMemsetAsync(A.Ucur, 0, size_t(nsub) * nw * sizeof(cplx), stream));
     SA.sparse_rhs = 1;
   }
-  const CheckArgs C = check_args(d_B, A.Ucur, A.zc, nullptr);
+  // steps >= 2: B is exactly zero off the transfer patches (cleared at step 2, only the
+  // patches rewritten since), so the check reads B there only
+  const CheckArgs C = check_args(d_B, A.Ucur, A.zc, nullptr, s >= 2);
   if (no_solve) {
     if (!(sskip & 4)) launch_check(C, stream);
   } else if (sskip & 4) {
@@ -1263,7 +1270,7 @@ void hddm_engine::enqueue_refine_body(int s, cudaStream_t stream, unsigned long 
   launch_refine_prep(R, stream);
   enqueue_solve(solve_args(d_R, d_C, d_Y, d_need, 1), stream);
   launch_refine_apply(R, stream);
-  launch_check_partials(check_args(d_B, A.Ucur, A.zc, d_need), stream);
+  launch_check_partials(check_args(d_B, A.Ucur, A.zc, d_need, s >= 2), stream);
   launch_refine_decide(R, stream);
   launch_refine_undo(R, stream);
 }

@@ -189,6 +189,8 @@ struct CheckArgs {
   int nsub;
   VMap vm;
   const cplx* B;
+  const unsigned char* bmask;  // per position: B may be nonzero (null: everywhere). Steps >= 2:
+                               // the transfer-patch union (B is exactly 0 elsewhere)
   const cplx* X;
   double* part;      // nsub x nchunk x 2
   int nchunk;

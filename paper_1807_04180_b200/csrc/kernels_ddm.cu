@@ -327,7 +327,7 @@ __device__ __forceinline__ void check_block(const CheckArgs& A, int c, int k0, i
         nb_n = __ldg(A.nbr + pn);
         k2_n = __ldg(k2c + pn);
       }
-      const cplx b = Bv[pos];
+      const cplx b = (A.bmask && !__ldg(A.bmask + pos)) ? cmk(0, 0) : Bv[pos];
       b2 += cnorm2(b);
       const cplx ax = ax_row_t(X, pos, A.wnx, A.wny, A.ih2, sa, k2, lq, nb);
       r2 += cnorm2(csub(b, ax));
