@@ -173,6 +173,10 @@ long long hddm_launch_count(const hddm_engine* e);
  * CUDA-graph launches on the engine stream; uses the right-hand sides of the
  * last sweep. hddm_solve_launches: kernels in that stage. */
 int hddm_time_solve(hddm_engine* e, int reps, double* ms_per_solve);
+/* Tuning aid: lane shape (E element lanes) of forward level `level` of the
+ * steady-state plan; which = 0/1 pulls of singleton / member tiles, 2/3 inverse
+ * rows; E = 0 restores the heuristic. Drops the cached step graphs. Process-wide. */
+int hddm_tune_fwd_shape(hddm_engine* e, int which, int level, int E);
 int hddm_solve_launches(const hddm_engine* e);
 /* Refinement diagnostics of the last call: the largest local-solve residual
  * ||b - A x||/||b|| seen (refine's first pass, sparse.cpp:268-292) and how many

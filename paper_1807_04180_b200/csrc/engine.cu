@@ -1905,6 +1905,18 @@ int hddm_time_solve(hddm_engine* e, int reps, double* ms_per_solve) {
 
 int hddm_solve_launches(const hddm_engine* e) { return solve_launch_count(e->plan); }
 
+int hddm_tune_fwd_shape(hddm_engine* e, int which, int level, int E) {
+  return guarded(e, [&] {
+    CK(cudaStreamSynchronize(e->st));
+    set_fwd_shape(which, level, E);
+    for (auto& g : e->step_exec)
+      if (g) {
+        CK(cudaGraphExecDestroy(g));
+        g = nullptr;
+      }
+  });
+}
+
 int hddm_refine_stats(const hddm_engine* e, double* max_local_relres, int* corrections) {
   *max_local_relres = e->last_max_rel;
   *corrections = e->last_refine_count;

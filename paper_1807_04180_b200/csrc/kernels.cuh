@@ -102,6 +102,9 @@ void launch_solve_group(const SolveArgs& A, const SolvePlan& P, int g, cudaStrea
 int solve_launch_count(const SolvePlan& P);  // kernels of one solve over all tiles
 void set_solve_skip(int mask, int only_tile);  // profiling aid (hddm_time_solve only)
 void set_solve_pdl(bool on);                  // programmatic dependent launch of the chains
+// forward lane-shape override of the steady-state plan (tuning): which = 0/1 pulls of
+// singleton / member tiles, 2/3 inverse rows; E = 0 restores the heuristic
+void set_fwd_shape(int which, int level, int E);
 
 // ------------------------------------------------------------------ factor
 struct FactorArgs {

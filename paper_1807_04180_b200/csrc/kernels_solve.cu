@@ -658,14 +658,58 @@ static int pow2_floor(long v) {
 
 // lanes per output for a forward pull/diagonal level with mean inner length avg
 // (defaults measured best at config 4; tuning knobs HDDM_FWD_DIV / HDDM_FWD_WIDE)
-static int fwd_lanes(int M, long avg, bool diag = false) {
-  static const long div_pull = std::getenv("HDDM_FWD_DIV") ? std::atol(std::getenv("HDDM_FWD_DIV")) : 32;
-  static const long div_diag = std::getenv("HDDM_DIAG_DIV") ? std::atol(std::getenv("HDDM_DIAG_DIV")) : 4;
-  const long div = diag ? div_diag : div_pull;
-  static const long wide = std::getenv("HDDM_FWD_WIDE") ? std::atol(std::getenv("HDDM_FWD_WIDE")) : 16;
+// Two parameter sets: the full-RHS plan (step 1, class solves; measured best at
+// config 4 with the full forward: HDDM_FWD_DIV 32, HDDM_FWD_WIDE 16) and the
+// steady-state sparse-RHS plan of steps >= 2 (tools/tune_fwd_shapes.py at config 4:
+// HDDM_FWD_DIV_SP 16, HDDM_FWD_WIDE_SP 6 -- 1.87 -> 1.73 ms per step; configs 1-3
+// gain 9-11 %).
+static long env_long(const char* name, long dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atol(v) : dflt;
+}
+
+static int fwd_lanes(int M, long avg, bool diag = false, bool sparse = false) {
+  static const long div_pull = env_long("HDDM_FWD_DIV", 32), div_pull_sp = env_long("HDDM_FWD_DIV_SP", 16);
+  static const long div_diag = env_long("HDDM_DIAG_DIV", 4);
+  static const long wide = env_long("HDDM_FWD_WIDE", 16), wide_sp = env_long("HDDM_FWD_WIDE_SP", 6);
+  const long div = diag ? div_diag : (sparse ? div_pull_sp : div_pull);
   if (M == 1) return std::max(1, std::min(32, pow2_floor(avg / div)));
-  if (avg > wide) return std::max(1, pow2_floor(32 / M));
+  if (avg > (sparse ? wide_sp : wide)) return std::max(1, pow2_floor(32 / M));
   return 1;
+}
+
+// Lane shape of a forward level: the heuristic fwd_lanes, or (tuning aid) a per-level
+// override for the steady-state (sparse-RHS) plan: HDDM_FWDP_E1 / HDDM_FWDP_EM (pulls of
+// singleton / member tiles) and HDDM_FWDD_E1 / HDDM_FWDD_EM (inverse rows), comma lists
+// of E per level (0: heuristic)
+static std::vector<int> g_fwd_tab[4];
+
+void set_fwd_shape(int which, int level, int E) {
+  if (which < 0 || which > 3 || level < 0 || level > 64) return;
+  std::vector<int>& t = g_fwd_tab[which];
+  if (int(t.size()) <= level) t.resize(level + 1, 0);
+  t[level] = E;
+}
+
+static int fwd_shape(int M, long avg, bool diag, bool sparse, int level) {
+  const int E = fwd_lanes(M, avg, diag, sparse);
+  if (!sparse) return E;
+  std::vector<int>* tab = g_fwd_tab;
+  static bool init = false;
+  if (!init) {
+    const char* names[4] = {"HDDM_FWDP_E1", "HDDM_FWDP_EM", "HDDM_FWDD_E1", "HDDM_FWDD_EM"};
+    for (int k = 0; k < 4; ++k)
+      if (const char* v = std::getenv(names[k]))
+        for (const char* q = v; *q;) {
+          tab[k].push_back(std::atoi(q));
+          while (*q && *q != ',') ++q;
+          if (*q) ++q;
+        }
+    init = true;
+  }
+  const std::vector<int>& t = tab[(diag ? 2 : 0) + (M > 1 ? 1 : 0)];
+  if (level < int(t.size()) && t[level] > 0 && t[level] * M <= 32) return t[level];
+  return E;
 }
 
 static TileArg with_shape(TileArg T, int E) {
@@ -733,13 +777,14 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
                    (const int2*)L.d_items, L.nitem);
       continue;
     }
+    const int li = int(&L - (sp ? P.fwd_sp.data() : P.fwd.data()));
     if (!(skip & 4)) {
-      const TileArg Tp = with_shape(T1, fwd_lanes(T1.M, L.avg_run));
+      const TileArg Tp = with_shape(T1, fwd_shape(T1.M, L.avg_run, false, sp, li));
       launch_pdl(k_fwd_pull, blocks(L.nitem, Tp.R), kThreads, 0, st, A, Tp, (const int4*)L.d_rec,
                  L.nitem);
     }
     if (!(skip & 8)) {
-      const TileArg Td = with_shape(T1, fwd_lanes(T1.M, L.avg_diag, true));
+      const TileArg Td = with_shape(T1, fwd_shape(T1.M, L.avg_diag, true, sp, li));
       launch_pdl(k_fwd_diag, blocks(L.nitem, Td.R), kThreads, 0, st, A, Td, (const int2*)L.d_items,
                  L.nitem);
     }

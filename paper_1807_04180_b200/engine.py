@@ -147,6 +147,7 @@ def load_library(path: str = LIB_PATH):
         "hddm_launch_count": (C.c_longlong, [vp]),
         "hddm_refine_stats": (C.c_int, [vp, dp, ip]),
         "hddm_time_solve": (C.c_int, [vp, C.c_int, dp]),
+        "hddm_tune_fwd_shape": (C.c_int, [vp, C.c_int, C.c_int, C.c_int]),
         "hddm_solve_launches": (C.c_int, [vp]),
         "hddm_stage_name": (C.c_char_p, [C.c_int]),
         "hddm_stream": (vp, [vp]),
@@ -425,6 +426,10 @@ class DdmEngine:
         ms = C.c_double()
         self._check(self.lib.hddm_time_solve(self.h, reps, C.byref(ms)))
         return ms.value
+
+    def tune_fwd_shape(self, which: int, level: int, lanes: int):
+        """Tuning aid: lane shape of a steady-state forward level (hddm_tune_fwd_shape)."""
+        self._check(self.lib.hddm_tune_fwd_shape(self.h, which, level, lanes))
 
     def solve_launches(self) -> int:
         return int(self.lib.hddm_solve_launches(self.h))
