@@ -473,6 +473,20 @@ static void solve_raw(const fact_t* F, const cplx* b, cplx* x) {
   for (int k = 0; k < n; ++k) x[F->perm[k]] = y[k];
 }
 
+/* diagnostics (test infrastructure): corrections taken and the largest first-pass
+ * relative residual since the last orc_refine_stats(reset) */
+static long g_ncorr = 0;
+static double g_maxrel = 0;
+
+void orc_refine_stats(long* ncorr, double* max_first_rel, int reset) {
+  if (ncorr) *ncorr = g_ncorr;
+  if (max_first_rel) *max_first_rel = g_maxrel;
+  if (reset) {
+    g_ncorr = 0;
+    g_maxrel = 0;
+  }
+}
+
 /* refine, sparse.cpp:268-292 */
 static double refine(const fact_t* F, const cplx* b, cplx* x) {
   const int n = F->n;
@@ -492,8 +506,10 @@ static double refine(const fact_t* F, const cplx* b, cplx* x) {
         for (int i = 0; i < n; ++i) x[i] -= F->cor[i];
       return r < rel ? r : rel;
     }
+    if (it == 0 && r > g_maxrel) g_maxrel = r;
     rel = r;
     if (rel <= 1e-11) return rel;
+    ++g_ncorr;
     solve_raw(F, F->res, F->cor);
     for (int i = 0; i < n; ++i) x[i] += F->cor[i];
   }

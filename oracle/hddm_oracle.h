@@ -86,6 +86,10 @@ int orc_class_solve(const orc_engine* e, int c, const double* b, double* x,
 int orc_window_dims(const orc_engine* e, int* nx, int* ny);
 int orc_nd_order(int nx, int ny, int* order);
 
+/* diagnostics: refinement corrections and largest first-pass relative residual since the
+ * last reset (test infrastructure) */
+void orc_refine_stats(long* ncorr, double* max_first_rel, int reset);
+
 #ifdef __cplusplus
 }
 #endif
