@@ -94,6 +94,13 @@ struct hddm_engine {
   int* d_pinv = nullptr;
   SolvePlan plan;
   cplx* d_vals = nullptr;
+  // separators solved by substitution (their diagonal blocks L_ss, row- and
+  // column-major packed, ncls x nlss each; lss_off per supernode, -1: inverse)
+  cplx* d_lss = nullptr;
+  cplx* d_lssc = nullptr;
+  long long* d_lss_off = nullptr;
+  long long nlss = 0;
+  std::vector<long long> h_lss_off;
   // per subdomain
   DevSub* d_sub = nullptr;
   cplx* d_sa = nullptr;
@@ -650,10 +657,40 @@ void hddm_engine::build_plan() {
       leaves.push_back(make_int2(s, 0));
       for (int j = 0; j < Y.sn[s].n; ++j) leafcols.push_back(make_int2(s, j));
     }
+  // Separators of SUBST_MIN..SUBST_MAX nodes are solved by substitution with L_ss
+  // itself; the larger and smaller ones by their explicit inverse (HDDM_SUBST_MIN /
+  // HDDM_SUBST_MAX; 0 / 0 switches substitution off)
+  {
+    const int smin = std::getenv("HDDM_SUBST_MIN") ? std::atoi(std::getenv("HDDM_SUBST_MIN")) : 24;
+    const int smax = std::min(256, std::getenv("HDDM_SUBST_MAX") ? std::atoi(std::getenv("HDDM_SUBST_MAX")) : 64);
+    std::vector<long long> off(Y.sn.size(), -1);
+    nlss = 0;
+    for (size_t s = 0; s < Y.sn.size(); ++s)
+      if (Y.sn[s].kind == 1 && Y.sn[s].n >= smin && Y.sn[s].n <= smax && smax > 0) {
+        off[s] = nlss;
+        nlss += (long long)Y.sn[s].n * (Y.sn[s].n - 1) / 2;
+      }
+    h_lss_off = off;
+    d_lss_off = upload(off);
+  }
   auto level = [&](const std::vector<int2>& v) {
     SolveLevel L;
     L.nitem = int(v.size());
     L.d_items = upload(v);
+    // the level's separators (items (s, 0)) for the substitution kernels
+    std::vector<int2> sp;
+    bool all = true;  // the substitution kernels replace a level's inverse kernel entirely
+    for (const int2& it : v)
+      if (it.y == 0 && Y.sn[it.x].kind == 1) {
+        if (h_lss_off[it.x] >= 0)
+          sp.push_back(it);
+        else
+          all = false;
+      }
+    if (!all) sp.clear();
+    L.nsep = int(sp.size());
+    for (const int2& it : sp) L.nmax_sep = std::max(L.nmax_sep, Y.sn[it.x].n);
+    if (L.nsep) L.d_seps = upload(sp);
     return L;
   };
   // leaves: w x h boxes in natural order; with the 5-point fill their band rows
@@ -941,6 +978,10 @@ void hddm_engine::factorize() {
   int* d_aj = upload(aent_j);
   int* d_ext = upload(Y.extadd);
   d_vals = dalloc<cplx>(size_t(ncls) * Y.nvals);
+  if (nlss > 0) {
+    d_lss = dalloc<cplx>(size_t(ncls) * nlss);
+    d_lssc = dalloc<cplx>(size_t(ncls) * nlss);
+  }
   CK(cudaMemsetAsync(d_vals, 0, size_t(ncls) * Y.nvals * sizeof(cplx), st));
   int* d_status = dalloc<int>(ncls);
   CK(cudaMemsetAsync(d_status, 0, sizeof(int) * ncls, st));
@@ -969,6 +1010,10 @@ void hddm_engine::factorize() {
     A.front_words = Y.front_words;
     A.vals = d_vals + size_t(c0) * Y.nvals;
     A.nvals = Y.nvals;
+    A.lss = d_lss ? d_lss + size_t(c0) * nlss : nullptr;
+    A.lssc = d_lssc ? d_lssc + size_t(c0) * nlss : nullptr;
+    A.lss_off = d_lss_off;
+    A.nlss = nlss;
     A.status = d_status + c0;
     for (size_t h = 0; h < lev.size(); ++h)
       if (!lev[h].empty()) launch_factor_level(A, d_lev[h], int(lev[h].size()), nb, st);
@@ -1002,6 +1047,10 @@ SolveArgs hddm_engine::solve_args(const cplx* Bp, cplx* X, cplx* Yp, const int* 
   A.bw = d_bw;
   A.vals = d_vals;
   A.nvals = Y.nvals;
+  A.lss = d_lss;
+  A.lssc = d_lssc;
+  A.lss_off = d_lss_off;
+  A.nlss = nlss;
   A.flag = flag;
   A.flag_on = on;
   A.sparse_rhs = 0;

@@ -23,6 +23,10 @@ struct SolveArgs {
   const SegRec* fseg;  // forward run segments of the plan in use (full or sparse RHS)
   const cplx* vals;    // ncls x nvals
   long long nvals;
+  const cplx* lss;     // null, or L_ss of the separators solved by substitution (row-major) ...
+  const cplx* lssc;    // ... and column-major packed (FactorArgs)
+  const long long* lss_off;
+  long long nlss;
   const int* flag;     // per RHS t: active iff (flag[t] != 0) == flag_on
   int flag_on;
   int sparse_rhs;      // host: RHS nonzero only on the transfer patches (forward plan fwd_sp)
@@ -69,6 +73,9 @@ struct SolveLevel {
   int nchunk4 = 0;
   int4* d_chunks4 = nullptr;
   int cw_max = 0;
+  // the level's separators (supernode, 0) for the substitution kernels
+  int nsep = 0, nmax_sep = 0;
+  int2* d_seps = nullptr;
 };
 
 struct SolvePlan {
@@ -121,6 +128,11 @@ struct FactorArgs {
   long long front_words;
   cplx* vals;         // ncls x nvals
   long long nvals;
+  cplx* lss;          // null, or ncls x nlss: diagonal blocks L_ss of the separators solved by
+                      // substitution (packed lower, row-major) ...
+  cplx* lssc;         // ... and column-major packed (column i: rows i+1..n-1)
+  const long long* lss_off;  // per supernode: offset of its block, -1: applied as an inverse
+  long long nlss;
   int* status;        // per class: 0 ok, 1 zero pivot
 };
 

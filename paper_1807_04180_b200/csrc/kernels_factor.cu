@@ -91,6 +91,16 @@ __global__ void __launch_bounds__(512) k_factor_node(FactorArgs A, const int* no
     // dense inverse of the unit-lower block, column j per thread:
     // X[i][j] = -(L[i][j] + sum_{q=j+1}^{i-1} L[i][q] X[q][j])
     cplx* Xp = vals + sn.diag_off;  // packed strictly lower, row-major
+    if (A.lss && A.lss_off[s] >= 0) {  // the block itself, row- and column-major packed
+      cplx* Lp = A.lss + (long long)blockIdx.y * A.nlss + A.lss_off[s];
+      cplx* Lc = A.lssc + (long long)blockIdx.y * A.nlss + A.lss_off[s];
+      for (int i = tid; i < n; i += nt)
+        for (int j = 0; j < i; ++j) {
+          const cplx v = F[(long long)i * Fn + j];
+          Lp[(long long)i * (i - 1) / 2 + j] = v;
+          Lc[(long long)j * (n - 1) - (long long)j * (j - 1) / 2 + (i - j - 1)] = v;
+        }
+    }
     for (int j = tid; j < n; j += nt) {
       for (int i = j + 1; i < n; ++i) {
         const cplx* Li = F + (long long)i * Fn;

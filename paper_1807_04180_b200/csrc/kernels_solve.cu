@@ -619,6 +619,97 @@ __global__ void __launch_bounds__(kThreads) k_bwd_leaf(SolveArgs A, TileArg T, c
   }
 }
 
+
+// Separator diagonal blocks by substitution with L_ss itself (the reference's
+// solve_raw order of operations, sparse.cpp:244-266) instead of an explicit
+// inverse: the inverse's rounding amplification pushed first-pass residuals over
+// refine's 1e-11 (config 4: 1.3e-11 with inverses, 5.5e-12 substituting, 8.2e-12
+// in the reference), and every crossing costs a whole correction solve.
+// A warp per (separator, member): lane l holds rows l, l+32, ... of the block in
+// registers; step i broadcasts the finished x_i from its owner lane and every lane
+// updates its rows below i with column i of L_ss (column-major packed: coalesced).
+// The backward (L^T) sweep runs j = n-1..0 with row j of L_ss (row-major packed).
+constexpr int kTrsvR = 2;  // rows per lane: separators up to 64 nodes
+
+// CTA per (tile, separator): the block (n(n-1)/2 entries, column-major for the
+// forward, row-major for the backward) is staged in shared memory once, then warp
+// k sweeps member k's right-hand side through it.
+template <bool BWD>
+__global__ void __launch_bounds__(512) k_sep_trsv(SolveArgs A, TileArg T, const int2* __restrict__ seps,
+                                                  int nsep) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  cplx* Ls = reinterpret_cast<cplx*>(smem);
+  const int lane = threadIdx.x & 31, k = threadIdx.x >> 5;
+  const int ti = blockIdx.x / nsep, is = blockIdx.x - ti * nsep;
+  const TileRec* rec = T.rec + ti;
+  const int s = seps[is].x;
+  const DevSn sn = A.sn[s];
+  const int n = sn.n, m = rec->m, M = T.M;
+  const long long nl = (long long)n * (n - 1) / 2;
+  const cplx* L = (BWD ? A.lss : A.lssc) + (long long)rec->c * A.nlss + A.lss_off[s];
+  for (long long e = threadIdx.x; e < nl; e += blockDim.x) Ls[e] = ldf(L + e);
+  __syncthreads();
+  if (k >= M) return;
+  if ((A.flag[rec->t[k]] != 0) != (A.flag_on != 0)) return;  // warp-uniform
+  const long long vb = rec->cb + k + (long long)sn.c0 * m;
+  cplx v[kTrsvR];
+#pragma unroll
+  for (int r = 0; r < kTrsvR; ++r) {
+    const int i = lane + 32 * r;
+    v[r] = i < n ? A.Y[vb + (long long)i * m] : cmk(0, 0);
+  }
+  if (!BWD) {
+#pragma unroll
+    for (int rs = 0; rs < kTrsvR; ++rs) {
+      if (32 * rs >= n) break;
+      for (int ii = 0; ii < 32; ++ii) {
+        const int i = 32 * rs + ii;
+        if (i >= n) break;
+        const cplx xi = cmk(__shfl_sync(0xffffffffu, v[rs].x, ii), __shfl_sync(0xffffffffu, v[rs].y, ii));
+        const cplx* col = Ls + (long long)i * (n - 1) - (long long)i * (i - 1) / 2 - (i + 1);  // col[kk] = L[kk][i]
+#pragma unroll
+        for (int r = rs; r < kTrsvR; ++r) {
+          const int kk = lane + 32 * r;
+          if (kk > i && kk < n) csub_mul(v[r], col[kk], xi);
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int rs = kTrsvR - 1; rs >= 0; --rs) {
+      if (32 * rs >= n) continue;
+      for (int jj = 31; jj >= 0; --jj) {
+        const int j = 32 * rs + jj;
+        if (j >= n) continue;
+        const cplx xj = cmk(__shfl_sync(0xffffffffu, v[rs].x, jj), __shfl_sync(0xffffffffu, v[rs].y, jj));
+        const cplx* row = Ls + (long long)j * (j - 1) / 2;  // row[i] = L[j][i], i < j
+#pragma unroll
+        for (int r = 0; r <= rs; ++r) {
+          const int i = lane + 32 * r;
+          if (i < j) csub_mul(v[r], row[i], xj);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kTrsvR; ++r) {
+    const int i = lane + 32 * r;
+    if (i < n) A.X[vb + (long long)i * m] = v[r];
+  }
+}
+
+template <bool BWD>
+static void launch_sep_trsv(const SolveArgs& A, const TileArg& T, const SolveLevel& L, cudaStream_t st) {
+  const size_t smem = size_t(L.nmax_sep) * (L.nmax_sep - 1) / 2 * sizeof(cplx);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sep_trsv<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_sep_trsv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    attr = true;
+  }
+  k_sep_trsv<BWD><<<unsigned(T.ntile * L.nsep), 32 * T.M, smem, st>>>(A, T, (const int2*)L.d_seps, L.nsep);
+}
+
 // ------------------------------------------------------------------ launcher
 int solve_launch_count(const SolvePlan& P) {
   return int(P.groups.size()) * (4 + 2 * int(P.fwd.size()) + 2 * int(P.bwd.size()));
@@ -748,6 +839,8 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
   if (g_only >= 0 && g != g_only) return;
   if (g_only <= -2 && P.groups[g].M != -2 - g_only) return;  // HDDM_ONLY_M (time_solve only)
   const TileArg T1 = with_shape(P.groups[g], 1);  // thread per (item, member)
+  // substitution for the mid-size separators: tiles of at least this many members
+  static const int subst_min_m = std::getenv("HDDM_SUBST_MIN_M") ? std::atoi(std::getenv("HDDM_SUBST_MIN_M")) : 2;
   const long long nt = T1.ntile;
   auto blocks = [nt](long long items, int R) { return blocks_for(nt * ((items + R - 1) / R) * 32); };
   // sparse RHS (steps >= 2): patch-free subtrees are skipped (z = 0, see zval)
@@ -783,7 +876,10 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
       launch_pdl(k_fwd_pull, blocks(L.nitem, Tp.R), kThreads, 0, st, A, Tp, (const int4*)L.d_rec,
                  L.nitem);
     }
-    if (!(skip & 8)) {
+    if (skip & 8) {
+    } else if (A.lss && L.nsep > 0 && T1.M >= subst_min_m) {
+      launch_sep_trsv<false>(A, T1, L, st);
+    } else {
       const TileArg Td = with_shape(T1, fwd_shape(T1.M, L.avg_diag, true, sp, li));
       launch_pdl(k_fwd_diag, blocks(L.nitem, Td.R), kThreads, 0, st, A, Td, (const int2*)L.d_items,
                  L.nitem);
@@ -809,6 +905,8 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
       launch_pdl(k_bwd_pull<false>, blocks(L.nitem, T1.R), kThreads, 0, st, A, T1,
                  (const int2*)L.d_items, L.nitem);
     if (skip & 32) {
+    } else if (A.lss && L.nsep > 0 && T1.M >= subst_min_m) {
+      launch_sep_trsv<true>(A, T1, L, st);
     } else if (L.split_diag && has_grp)
       launch_pdl(k_bwd_split<true>, gs, kSplitWarps * 32, 0, st, A, T1, (const int2*)grp->second.second,
                  grp->second.first);
