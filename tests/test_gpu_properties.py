@@ -190,3 +190,33 @@ def test_single_subdomain_is_a_direct_solve():
         e.solve_iterative(prob.source_f(), 1e-10, 5, st)
         assert st.steps == 1 and st.solves == 1 and st.skipped == 0
         assert st.converged and st.relres <= 1e-12
+
+
+@pytest.mark.gpu
+def test_separator_substitution_matches_inverse_path(monkeypatch):
+    """The 24-64-node separators of member tiles are solved by substitution with L_ss
+    (accuracy: first-pass residuals stay under refine's 1e-11); switching it off
+    (HDDM_SUBST_MAX=0, read when the plan is built) applies every separator as an
+    explicit inverse. Both give the same sweeps to rounding and the same solve / skip
+    counts; at config 4 the substitution path needs no correction pass."""
+    from paper_1807_04180_b200.engine import DdmEngine, DdmStats
+    from paper_1807_04180_b200.problems import config
+    prob = config(2)
+    r = interior_random(prob, 5)
+    monkeypatch.delenv("HDDM_SUBST_MAX", raising=False)
+    with DdmEngine(prob) as a:
+        sa = DdmStats()
+        za = a.precondition(r, 4, sa)
+    monkeypatch.setenv("HDDM_SUBST_MAX", "0")
+    with DdmEngine(prob) as b:
+        sb = DdmStats()
+        zb = b.precondition(r, 4, sb)
+    monkeypatch.delenv("HDDM_SUBST_MAX", raising=False)
+    assert rel_l2(za, zb) <= 1e-10
+    assert (sa.solves, sa.skipped) == (sb.solves, sb.skipped)
+    prob4 = config(4)
+    with DdmEngine(prob4) as e:
+        e.set_timing(True)
+        e.precondition(interior_random(prob4, 7), 8)
+        max_rel, corrections = e.refine_stats()
+    assert corrections == 0 and max_rel < 1e-11, (max_rel, corrections)
