@@ -8,7 +8,7 @@ import json
 import sys
 
 SOLVE = ("k_ring", "k_fwd_leaf", "k_fwd_pull", "k_fwd_diag", "k_bwd_stage", "k_bwd_pull",
-         "k_bwd_diag", "k_bwd_split", "k_bwd_leaf")
+         "k_bwd_diag", "k_bwd_split", "k_bwd_leaf", "k_sep_trsv")
 
 
 def load(path):
