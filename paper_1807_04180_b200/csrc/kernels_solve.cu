@@ -751,9 +751,9 @@ static int pow2_floor(long v) {
 // (defaults measured best at config 4; tuning knobs HDDM_FWD_DIV / HDDM_FWD_WIDE)
 // Two parameter sets: the full-RHS plan (step 1, class solves; measured best at
 // config 4 with the full forward: HDDM_FWD_DIV 32, HDDM_FWD_WIDE 16) and the
-// steady-state sparse-RHS plan of steps >= 2 (tools/tune_fwd_shapes.py at config 4:
-// HDDM_FWD_DIV_SP 16, HDDM_FWD_WIDE_SP 6 -- 1.87 -> 1.73 ms per step; configs 1-3
-// gain 9-11 %).
+// steady-state sparse-RHS plan of steps >= 2 (config 4: HDDM_FWD_DIV_SP 16 against 32,
+// 1.81 -> 1.75 ms per step; per-level tuning with tools/tune_fwd_shapes.py finds no
+// better point).
 static long env_long(const char* name, long dflt) {
   const char* v = std::getenv(name);
   return v ? std::atol(v) : dflt;
