@@ -133,6 +133,11 @@ int hddm_fgmres(hddm_engine* e, const double* b, double* x, double tol,
 
 /* ---- parity / measurement taps (not part of the reference surface) ---- */
 
+/* Z_j = M(V_j) of the last FGMRES restart cycle of hddm_fgmres (j < the cycle's
+ * usable columns), n_global() complex -- the preconditioned vectors the reference's
+ * fgmres keeps (krylov.cpp:59-63), for per-iteration parity. */
+int hddm_fgmres_z(hddm_engine* e, int j, double* out, int memkind);
+
 /* After the last sweep: subdomain t's scaled right-hand side and solution in
  * window-local natural order (n_w complex each) and its active flag. */
 int hddm_tap_subdomain(hddm_engine* e, int t, double* rhs, double* u,

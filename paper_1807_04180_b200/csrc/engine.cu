@@ -182,6 +182,18 @@ struct hddm_engine {
   cplx* d_b = nullptr;
   cplx* d_x = nullptr;
   cplx* d_r = nullptr;
+  cplx** d_Vptr = nullptr;
+  KryState* d_ks = nullptr;
+  KryState* h_ks = nullptr;  // pinned mirror
+  double* d_hist = nullptr;  // recursive relres per FGMRES iteration
+  int d_hist_cap = 0;
+  int kry_k_last = 0;        // usable columns of the last FGMRES cycle (Z_j taps)
+  cudaGraphExec_t kry_exec = nullptr;  // one restart cycle: WHILE over Arnoldi iterations
+  int kry_K = -1, kry_iter_kernels = 0;
+  KryArgs kry_args(unsigned long long cond);
+  int enqueue_kry_iteration(int K, unsigned long long cond, cudaGraph_t body);
+  void build_kry_graph(int K);
+  void launch_kry_cycle(int K, int m);
 
   template <class T>
   T* dalloc(size_t n) {
@@ -209,6 +221,8 @@ struct hddm_engine {
     for (void* p : allocs) cudaFree(p);
     for (auto& e : ev_pool) cudaEventDestroy(e);
     if (h_scal) cudaFreeHost(h_scal);
+    if (h_ks) cudaFreeHost(h_ks);
+    if (kry_exec) cudaGraphExecDestroy(kry_exec);
     for (auto& g : step_exec)
       if (g) cudaGraphExecDestroy(g);
     for (ForkSet* F : {&fork_main, &fork_body}) {
@@ -256,6 +270,7 @@ struct hddm_engine {
   void enqueue_step_front(int s, cudaStream_t stream, unsigned long long cond);
   void enqueue_refine_body(int s, cudaStream_t stream, unsigned long long cond);
   void build_step_graph(int v);
+  int capture_step(int s, cudaGraph_t g);
   void run_step(int s);
   void host_refine(const cplx* Bp, cplx* X, const int* zc);
   void reset_state();
@@ -344,6 +359,7 @@ void hddm_engine::create(const hddm_problem& p) {
   CK(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
   per_class_streams = std::getenv("HDDM_SINGLE_STREAM") == nullptr;
   CK(cudaMallocHost(&h_scal, 64 * sizeof(double)));
+  CK(cudaMallocHost(&h_ks, sizeof(KryState)));
   nsub = S.n1 * S.n2;
   ncls = S.ncls;
   wnx = S.subs[0].nx;
@@ -662,7 +678,8 @@ void hddm_engine::build_plan() {
   // HDDM_SUBST_MAX; 0 / 0 switches substitution off)
   {
     const int smin = std::getenv("HDDM_SUBST_MIN") ? std::atoi(std::getenv("HDDM_SUBST_MIN")) : 24;
-    const int smax = std::min(256, std::getenv("HDDM_SUBST_MAX") ? std::atoi(std::getenv("HDDM_SUBST_MAX")) : 64);
+    // k_sep_trsv keeps 32 * kTrsvR = 64 rows per warp in registers
+    const int smax = std::min(64, std::getenv("HDDM_SUBST_MAX") ? std::atoi(std::getenv("HDDM_SUBST_MAX")) : 64);
     std::vector<long long> off(Y.sn.size(), -1);
     nlss = 0;
     for (size_t s = 0; s < Y.sn.size(); ++s)
@@ -1329,13 +1346,12 @@ void hddm_engine::enqueue_refine_body(int s, cudaStream_t stream, unsigned long 
 static int variant_of(int s) { return s == 1 ? 0 : (s == 2 ? 4 : 1 + (s % 3)); }
 static int rep_step(int v) { return v == 0 ? 1 : (v == 1 ? 3 : (v == 2 ? 4 : (v == 3 ? 5 : 2))); }
 
-void hddm_engine::build_step_graph(int v) {
-  const int s = rep_step(v);
-  cudaGraph_t g;
-  CK(cudaGraphCreate(&g, 0));
+// One DDM step (flags, RHS, solve + first residual check, the refinement WHILE node,
+// accumulate) captured onto st, which must be capturing into graph g. Returns the
+// number of kernels the step launches when no correction pass runs.
+int hddm_engine::capture_step(int s, cudaGraph_t g) {
   cudaGraphConditionalHandle h;
   CK(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
-  CK(cudaStreamBeginCaptureToGraph(st, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   enqueue_step_front(s, st, (unsigned long long)h);
   cudaStreamCaptureStatus cs;
   const cudaGraphNode_t* deps = nullptr;
@@ -1354,17 +1370,22 @@ void hddm_engine::build_step_graph(int v) {
   enqueue_refine_body(s, st2, (unsigned long long)h);
   cudaGraph_t bout;
   CK(cudaStreamEndCapture(st2, &bout));
-  static const int sskip = std::getenv("HDDM_STEP_SKIP") ? std::atoi(std::getenv("HDDM_STEP_SKIP")) : 0;
-  if (!(sskip & 8)) launch_accumulate(step_args(s, d_f), st);
+  launch_accumulate(step_args(s, d_f), st);
+  // flags, RHS (base + transfer at step 1; after it B is cleared by a memset),
+  // the solve, check + finish/refine-init, accumulate
+  return 1 + (s == 1 ? 2 : 1) + solve_launches() + 2 + 1;
+}
+
+void hddm_engine::build_step_graph(int v) {
+  const int s = rep_step(v);
+  cudaGraph_t g;
+  CK(cudaGraphCreate(&g, 0));
+  CK(cudaStreamBeginCaptureToGraph(st, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  step_kernels[v] = capture_step(s, g);
   cudaGraph_t gout;
   CK(cudaStreamEndCapture(st, &gout));
   CK(cudaGraphInstantiate(&step_exec[v], g, 0));
   CK(cudaGraphDestroy(g));
-  // kernels per step when no correction runs: flags, 2 RHS, solve, check (2),
-  // refine init, accumulate
-  // flags, RHS (base + transfer at step 1; after it B is cleared by a memset),
-  // the solve, check + finish/refine-init, accumulate
-  step_kernels[v] = 1 + (s == 1 ? 2 : 1) + solve_launches() + 2 + 1;
 }
 
 void hddm_engine::run_step(int s) {
@@ -1431,6 +1452,14 @@ void hddm_engine::ensure_krylov(int m) {
   if (d_Zptr) dfree(d_Zptr);
   d_Zptr = dalloc<cplx*>(m);
   CK(cudaMemcpyAsync(d_Zptr, Z.data(), sizeof(cplx*) * m, cudaMemcpyHostToDevice, st));
+  if (d_Vptr) dfree(d_Vptr);
+  d_Vptr = dalloc<cplx*>(m + 1);
+  CK(cudaMemcpyAsync(d_Vptr, V.data(), sizeof(cplx*) * (m + 1), cudaMemcpyHostToDevice, st));
+  if (!d_ks) d_ks = dalloc<KryState>(1);
+  if (kry_exec) {  // the cycle graph holds the old buffers
+    CK(cudaGraphExecDestroy(kry_exec));
+    kry_exec = nullptr;
+  }
   for (cplx* p : {d_H, d_g, d_sn_g, d_y})
     if (p) dfree(p);
   if (d_cs) dfree(d_cs);
@@ -1445,6 +1474,100 @@ void hddm_engine::ensure_krylov(int m) {
     d_r = dalloc<cplx>(ng);
   }
   kry_m = m;
+  CK(cudaStreamSynchronize(st));
+}
+
+KryArgs hddm_engine::kry_args(unsigned long long cond) {
+  KryArgs K;
+  K.ks = d_ks;
+  K.V = d_Vptr;
+  K.Z = d_Zptr;
+  K.H = d_H;
+  K.ld = kry_m + 1;
+  K.g = d_g;
+  K.sn = d_sn_g;
+  K.cs = d_cs;
+  K.hist = d_hist;
+  K.part = d_part;
+  K.n = ng;
+  K.cond = cond;
+  return K;
+}
+
+// One Arnoldi iteration of fgmres (krylov.cpp:57-109) with the column index j on the
+// device: Z_j = M(V_j) (K DDM steps), w = A Z_j, modified Gram-Schmidt (unrolled to
+// the cycle length; steps beyond j exit at once), Givens, V_{j+1} = w / hlast.
+// body != null: captured into that graph (step graphs inline); else launched
+// directly (HDDM_NO_GRAPHS profiling path). Returns the kernels one iteration runs.
+int hddm_engine::enqueue_kry_iteration(int K, unsigned long long cond, cudaGraph_t body) {
+  const KryArgs KA = kry_args(cond);
+  int nk = 0;
+  reset_state();
+  nk += 3;
+  launch_kry_load(KA, d_f, st);
+  launch_fany(step_args(1, d_f), st);
+  nk += 2;
+  for (int s = 1; s <= K; ++s) {
+    if (body)
+      nk += capture_step(s, body);
+    else
+      run_step(s);
+  }
+  launch_kry_store(KA, d_asm, st);
+  GlobalArgs G{S.gnx, S.gny, 1.0 / (S.h * S.h), d_ga, d_k2};
+  launch_apply_global_ind(G, d_Zptr, 0, d_Vptr, 1, &d_ks->j, st);
+  launch_kry_first_dot(KA, st);
+  nk += 4;
+  for (int i = 0; i < kry_m; ++i) launch_kry_mgs(KA, i, st);
+  nk += 2 * kry_m;
+  launch_kry_givens(KA, st);
+  launch_kry_next(KA, st);
+  nk += 3;
+  return nk;
+}
+
+void hddm_engine::build_kry_graph(int K) {
+  if (kry_exec) {
+    CK(cudaGraphExecDestroy(kry_exec));
+    kry_exec = nullptr;
+  }
+  cudaGraph_t G;
+  CK(cudaGraphCreate(&G, 0));
+  cudaGraphConditionalHandle hc;
+  CK(cudaGraphConditionalHandleCreate(&hc, G, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = hc;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t wn;
+  CK(cudaGraphAddNode(&wn, G, nullptr, 0, &cp));
+  cudaGraph_t B = cp.conditional.phGraph_out[0];
+  CK(cudaStreamBeginCaptureToGraph(st, B, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  kry_iter_kernels = enqueue_kry_iteration(K, (unsigned long long)hc, B);
+  cudaGraph_t out;
+  CK(cudaStreamEndCapture(st, &out));
+  CK(cudaGraphInstantiate(&kry_exec, G, 0));
+  CK(cudaGraphDestroy(G));
+  kry_K = K;
+}
+
+// The Arnoldi iterations of one restart cycle (state in d_ks, set by the caller).
+void hddm_engine::launch_kry_cycle(int K, int m) {
+  (void)m;
+  static const bool no_graphs = std::getenv("HDDM_NO_GRAPHS") != nullptr;
+  if (no_graphs) {  // host-driven (profiling): one sync per iteration
+    for (;;) {
+      enqueue_kry_iteration(K, 0, nullptr);
+      CK(cudaMemcpyAsync(h_ks, d_ks, sizeof(KryState), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      launches += 6 + 2 * kry_m;
+      if (!h_ks->adv) break;
+    }
+    return;
+  }
+  if (!kry_exec || kry_K != K) build_kry_graph(K);
+  CK(cudaGraphLaunch(kry_exec, st));
 }
 
 // ----------------------------------------------------------------- C-ABI
@@ -1496,10 +1619,6 @@ void check_refine(hddm_engine* e) {
   CK(cudaStreamSynchronize(e->st));
   e->last_max_rel = mx;
   e->last_refine_count = flag;  // solves whose first pass exceeded 1e-11 (corrected on device)
-  if (false)
-    throw SolveErr(
-        "a local solve needed iterative-refinement corrections (relres > 1e-11); "
-        "correction passes are not implemented on the GPU path");
 }
 
 }  // namespace
@@ -1599,6 +1718,7 @@ int hddm_solve_iterative(hddm_engine* e, const double* f, double tol, int max_st
     e->reset_state();
     CK(cudaMemsetAsync(e->d_counts, 0, 2 * sizeof(long long), e->st));
     CK(cudaMemsetAsync(e->d_refine, 0, sizeof(int), e->st));
+    CK(cudaMemsetAsync(e->d_maxrel, 0, sizeof(double), e->st));
     if (bnorm == 0) {
       st.converged = 1;
       st.relres = 0;
@@ -1693,96 +1813,80 @@ int hddm_fgmres(hddm_engine* e, const double* b, double* x, double tol, int max_
                        memkind == HDDM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(e->d_x, 0, n * sizeof(cplx), st));
     CK(cudaMemsetAsync(e->d_refine, 0, sizeof(int), st));
+    CK(cudaMemsetAsync(e->d_maxrel, 0, sizeof(double), st));
+    CK(cudaMemsetAsync(e->d_counts, 0, 2 * sizeof(long long), st));
     const double bnorm = e->device_norm(e->d_b);
     GlobalArgs G{e->S.gnx, e->S.gny, 1.0 / (e->S.h * e->S.h), e->d_ga, e->d_k2};
-    long long cnt_solves = 0, cnt_skipped = 0;
     double sweep_ms = 0;
+    e->kry_k_last = 0;
+    if (e->d_hist_cap < max_iters) {  // the cycle graph holds the old buffer
+      if (e->d_hist) e->dfree(e->d_hist);
+      e->d_hist_cap = std::max(max_iters, 256);
+      e->d_hist = e->dalloc<double>(e->d_hist_cap);
+      if (e->kry_exec) {
+        CK(cudaGraphExecDestroy(e->kry_exec));
+        e->kry_exec = nullptr;
+      }
+    }
     if (bnorm == 0) {
       R.converged = 1;
       R.relres = R.true_relres = 0;
     } else {
       CK(cudaMemcpyAsync(e->d_r, e->d_b, n * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-      int total = 0;
-      bool stop = false;
-      while (!stop && total < max_iters) {
-        const int m = restart > 0 ? std::min(restart, max_iters - total) : max_iters - total;
+      KryState ks{};
+      ks.total = 0;
+      ks.max_iters = max_iters;
+      ks.tol = tol;
+      ks.bnorm = bnorm;
+      while (!ks.stop && ks.total < max_iters) {
+        const int m = restart > 0 ? std::min(restart, max_iters - ks.total) : max_iters - ks.total;
         const double rnorm = e->device_norm(e->d_r);
         if (rnorm == 0) {
-          R.converged = 1;
+          ks.converged = 1;
           break;
         }
+        // one restart cycle: V_0 = r / |r|, g = |r| e_0, then the Arnoldi iterations
+        // as ONE graph launch (WHILE node, status on the device); the host reads the
+        // cycle's status record once (krylov.cpp:53-109)
         e->h_scal[8] = rnorm;
         CK(cudaMemcpyAsync(e->d_scal + 8, e->h_scal + 8, sizeof(double), cudaMemcpyHostToDevice, st));
         launch_scale_div(e->V[0], e->d_r, e->d_scal + 8, n, st);
         launch_init_g(e->d_g, m, e->d_scal + 8, st);
         CK(cudaMemsetAsync(e->d_H, 0, sizeof(cplx) * size_t(mcap) * ld, st));
-        int k = 0;
-        for (int j = 0; j < m; ++j) {
-          const double it0 = now_ms();
-          // Z_j = M(V_j): K DDM sweeps (precondition, ddm.cpp:280-287)
-          e->reset_state();
-          CK(cudaMemsetAsync(e->d_counts, 0, 2 * sizeof(long long), st));
-          CK(cudaMemcpyAsync(e->d_f, e->V[j], n * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-          StepArgs A0 = e->step_args(1, e->d_f);
-          launch_fany(A0, st);
-          const double ts = now_ms();
-          for (int s = 1; s <= ksteps; ++s) e->run_step(s);
-          CK(cudaMemcpyAsync(e->Z[j], e->d_asm, n * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-          // w = A Z_j
-          cplx* w = e->V[j + 1];
-          launch_apply_global(G, e->Z[j], w, nullptr, nullptr, st);
-          // MGS: h_0j, then fused (axpy_i, dot_{i+1} | norm)
-          cplx* Hc = e->d_H + size_t(j) * ld;
-          launch_dot_part(e->V[0], w, n, e->d_part, st);
-          launch_finish_sum(e->d_part, 2, reinterpret_cast<double*>(Hc), st);
-          for (int i = 0; i <= j; ++i) {
-            const cplx* Vn = i < j ? e->V[i + 1] : nullptr;
-            launch_axpy_dot(w, e->V[i], Hc + i, Vn, n, e->d_part, st);
-            if (Vn)
-              launch_finish_sum(e->d_part, 2, reinterpret_cast<double*>(Hc + i + 1), st);
-            else
-              launch_finish_sum(e->d_part, 1, e->d_scal + 4, st);  // |w|^2
-          }
-          launch_givens(Hc, e->d_scal + 4, e->d_cs, e->d_sn_g, e->d_g, j, bnorm, e->d_scal + 16,
-                        e->d_scal + 5, st);
-          CK(cudaMemcpyAsync(e->h_scal + 16, e->d_scal + 16, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
-          long long cnt[2];
-          CK(cudaMemcpyAsync(cnt, e->d_counts, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st));
-          CK(cudaStreamSynchronize(st));
-          cnt_solves += cnt[0];
-          cnt_skipped += cnt[1];
-          sweep_ms += now_ms() - ts;
-          const int flags = int(e->h_scal[17]);
-          if (flags & 1) {  // dead column
-            stop = true;
-            break;
-          }
-          ++total;
-          k = j + 1;
-          R.relres = e->h_scal[16];
-          if (hist && total - 1 < hist_cap) hist[total - 1] = R.relres;
-          (void)it0;
-          if (R.relres <= tol) {
-            R.converged = 1;
-            stop = true;
-            break;
-          }
-          if (flags & 2) {  // hlast == 0
-            stop = true;
-            break;
-          }
-          launch_scale_div(w, w, e->d_scal + 5, n, st);
+        ks.j = 0;
+        ks.m = m;
+        ks.k = 0;
+        ks.adv = 0;
+        *e->h_ks = ks;
+        CK(cudaMemcpyAsync(e->d_ks, e->h_ks, sizeof(KryState), cudaMemcpyHostToDevice, st));
+        const double ts = now_ms();
+        e->launch_kry_cycle(ksteps, m);
+        CK(cudaMemcpyAsync(e->h_ks, e->d_ks, sizeof(KryState), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        sweep_ms += now_ms() - ts;
+        const int before = ks.total;
+        ks = *e->h_ks;
+        if (e->kry_exec)  // iterations run by the cycle graph (a dead column runs too)
+          e->launches += (long long)e->kry_iter_kernels * (ks.total - before + (ks.flags & 1));
+        if (hist) {
+          const int lo = std::min(before, hist_cap), hi = std::min(ks.total, hist_cap);
+          if (hi > lo)
+            CK(cudaMemcpy(hist + lo, e->d_hist + lo, sizeof(double) * (hi - lo), cudaMemcpyDeviceToHost));
         }
+        if (ks.total > before) R.relres = ks.relres;
+        const int k = ks.k;
+        e->kry_k_last = k;
         if (k > 0) {
           launch_backsolve(e->d_H, ld, e->d_g, e->d_y, k, st);
           launch_update_x(e->d_x, e->d_Zptr, e->d_y, k, n, st);
         }
-        if (!stop) {
+        if (!ks.stop) {  // restart: the residual recomputed explicitly
           launch_apply_global(G, e->d_x, e->d_r, nullptr, nullptr, st);
           launch_bsub(e->d_r, e->d_b, n, st);
         }
       }
-      R.iters = total;
+      R.iters = ks.total;
+      R.converged = ks.converged;
       // true residual, krylov.cpp:126-131
       launch_apply_global(G, e->d_x, nullptr, e->d_b, e->d_part, st);
       launch_finish_sum(e->d_part, 1, e->d_scal, st);
@@ -1791,16 +1895,25 @@ int hddm_fgmres(hddm_engine* e, const double* b, double* x, double tol, int max_
       R.true_relres = std::sqrt(e->h_scal[0]) / bnorm;
     }
     out_copy(e, x, e->d_x, memkind);
-    CK(cudaStreamSynchronize(st));
+    long long cnt[2];
+    read_counts(e, cnt);
     check_refine(e);
     R.wall_ms = now_ms() - tstart;
     if (res) *res = R;
     if (pstats) {
-      pstats->solves += long(cnt_solves);
-      pstats->skipped += long(cnt_skipped);
+      pstats->solves += long(cnt[0]);
+      pstats->skipped += long(cnt[1]);
       pstats->sweep_ms += sweep_ms;
       pstats->factor_ms = e->factor_ms;
     }
+  });
+}
+
+int hddm_fgmres_z(hddm_engine* e, int j, double* out, int memkind) {
+  return guarded(e, [&] {
+    if (j < 0 || j >= e->kry_k_last) throw ConfigErr("no such preconditioned vector Z_j (last FGMRES cycle)");
+    out_copy(e, out, e->Z[j], memkind);
+    CK(cudaStreamSynchronize(e->st));
   });
 }
 
@@ -1963,6 +2076,10 @@ int hddm_tune_fwd_shape(hddm_engine* e, int which, int level, int E) {
         CK(cudaGraphExecDestroy(g));
         g = nullptr;
       }
+    if (e->kry_exec) {
+      CK(cudaGraphExecDestroy(e->kry_exec));
+      e->kry_exec = nullptr;
+    }
   });
 }
 

@@ -9,6 +9,9 @@
 
 namespace hddm {
 
+// fixed grid of the reduction kernels (4 x 148 SMs) => fixed summation order
+constexpr int kReduceBlocks = 592;
+
 // ------------------------------------------------------------------ solves
 struct SolveArgs {
   const DevSn* sn;
@@ -274,6 +277,9 @@ struct GlobalArgs {
 // out = L u (ring identity); if f != nullptr also partial sums of |f - out|^2
 void launch_apply_global(const GlobalArgs& G, const cplx* u, cplx* out, const cplx* f,
                          double* part, cudaStream_t st);
+// the same with u = U[*jp + du], out = O[*jp + dout] (device-resident Krylov index j)
+void launch_apply_global_ind(const GlobalArgs& G, cplx* const* U, int du, cplx* const* O, int dout,
+                             const int* jp, cudaStream_t st);
 int reduce_blocks();  // number of partials the reduction kernels produce
 
 // deterministic reductions / BLAS-1 over n complex

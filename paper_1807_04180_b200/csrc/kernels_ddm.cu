@@ -17,7 +17,7 @@ namespace hddm {
 
 namespace {
 
-constexpr int kRedBlocks = 592;  // 4 x 148 SMs: fixed grid => fixed summation order
+constexpr int kRedBlocks = kReduceBlocks;
 __constant__ int kDI[8] = {+1, -1, 0, 0, +1, -1, +1, -1};  // source offsets in
 __constant__ int kDJ[8] = {0, 0, +1, -1, +1, +1, -1, -1};  // kGatherOrder L,R,D,U,DL,DR,UL,UR
 
@@ -575,8 +575,8 @@ void launch_refine_undo(const RefineArgs& R, cudaStream_t st) {
 // ------------------------------------------------------------ global stencil
 // DiscreteOperator::apply (discretize.cpp:81-96) on the global window; when f is
 // given, also per-block partial sums of |f - L u|^2 (residual_norm, ddm.cpp:237-242).
-__global__ void __launch_bounds__(256) k_apply_global(GlobalArgs G, const cplx* u, cplx* out,
-                                                      const cplx* f, double* part) {
+__device__ __forceinline__ void apply_global_body(const GlobalArgs& G, const cplx* u, cplx* out,
+                                                  const cplx* f, double* part) {
   __shared__ double sh[32];
   const long long n = (long long)G.gnx * G.gny;
   const cplx* a1n = G.ga;
@@ -609,9 +609,26 @@ __global__ void __launch_bounds__(256) k_apply_global(GlobalArgs G, const cplx* 
   }
 }
 
+__global__ void __launch_bounds__(256) k_apply_global(GlobalArgs G, const cplx* u, cplx* out,
+                                                      const cplx* f, double* part) {
+  apply_global_body(G, u, out, f, part);
+}
+
+// out = L u with u = U[*jp + du], out = O[*jp + dout] (device-resident Krylov index)
+__global__ void __launch_bounds__(256) k_apply_global_ind(GlobalArgs G, cplx* const* U, int du,
+                                                          cplx* const* O, int dout, const int* jp) {
+  const int j = *jp;
+  apply_global_body(G, U[j + du], O[j + dout], nullptr, nullptr);
+}
+
 void launch_apply_global(const GlobalArgs& G, const cplx* u, cplx* out, const cplx* f,
                          double* part, cudaStream_t st) {
   k_apply_global<<<kRedBlocks, 256, 0, st>>>(G, u, out, f, part);
+}
+
+void launch_apply_global_ind(const GlobalArgs& G, cplx* const* U, int du, cplx* const* O, int dout,
+                             const int* jp, cudaStream_t st) {
+  k_apply_global_ind<<<kRedBlocks, 256, 0, st>>>(G, U, du, O, dout, jp);
 }
 
 // ------------------------------------------------------------ reductions

@@ -877,7 +877,7 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
                  L.nitem);
     }
     if (skip & 8) {
-    } else if (A.lss && L.nsep > 0 && T1.M >= subst_min_m) {
+    } else if (A.lss && L.nsep > 0 && T1.M >= subst_min_m && T1.M <= 16) {
       launch_sep_trsv<false>(A, T1, L, st);
     } else {
       const TileArg Td = with_shape(T1, fwd_shape(T1.M, L.avg_diag, true, sp, li));
@@ -905,7 +905,7 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
       launch_pdl(k_bwd_pull<false>, blocks(L.nitem, T1.R), kThreads, 0, st, A, T1,
                  (const int2*)L.d_items, L.nitem);
     if (skip & 32) {
-    } else if (A.lss && L.nsep > 0 && T1.M >= subst_min_m) {
+    } else if (A.lss && L.nsep > 0 && T1.M >= subst_min_m && T1.M <= 16) {
       launch_sep_trsv<true>(A, T1, L, st);
     } else if (L.split_diag && has_grp)
       launch_pdl(k_bwd_split<true>, gs, kSplitWarps * 32, 0, st, A, T1, (const int2*)grp->second.second,

@@ -106,6 +106,7 @@ class FgmresResult:
 
 
 _lib = None
+_OPTIONAL = {"hddm_fgmres_z"}
 
 
 def load_library(path: str = LIB_PATH):
@@ -135,6 +136,7 @@ def load_library(path: str = LIB_PATH):
         "hddm_precondition": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, P(_Stats)]),
         "hddm_fgmres": (C.c_int, [vp, vp, vp, d, C.c_int, C.c_int, C.c_int, C.c_int,
                                   P(_FgRes), dp, C.c_int, P(_Stats)]),
+        "hddm_fgmres_z": (C.c_int, [vp, C.c_int, vp, C.c_int]),
         "hddm_tap_subdomain": (C.c_int, [vp, C.c_int, dp, dp, ip]),
         "hddm_class_solve": (C.c_int, [vp, C.c_int, dp, dp, dp]),
         "hddm_window_dims": (C.c_int, [vp, ip, ip]),
@@ -153,6 +155,8 @@ def load_library(path: str = LIB_PATH):
         "hddm_stream": (vp, [vp]),
     }
     for name, (res, args) in sigs.items():
+        if name in _OPTIONAL and not hasattr(lib, name):
+            continue  # an older build (tools/ comparisons only)
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
@@ -287,6 +291,8 @@ class DdmEngine:
             return C.c_void_p(a.data_ptr()), HDDM_DEVICE, a
         arr = np.asarray(a)
         if arr.dtype != np.complex128 or not arr.flags.c_contiguous or (writable and not arr.flags.writeable):
+            if writable:  # results must land in the caller's array, not in a copy
+                raise ConfigError("output arrays must be writable C-contiguous complex128")
             arr = np.ascontiguousarray(arr, dtype=np.complex128)
         if arr.size != self.n:
             raise SolveError("source vector size mismatch")
@@ -339,7 +345,9 @@ class DdmEngine:
         """z = M(r) with K sweeps (ddm.hpp:78); counts accumulate into stats."""
         pr, mk, keep = self._io(r)
         z = self._out_like(r) if out is None else out
-        pz, _, keep2 = self._io(z, writable=True)
+        pz, mk2, keep2 = self._io(z, writable=True)
+        if mk != mk2:
+            raise ConfigError("r and out must live in the same memory")
         st = _Stats()
         if stats is not None:
             st.solves, st.skipped, st.sweep_ms = stats.solves, stats.skipped, stats.sweep_ms
@@ -371,6 +379,12 @@ class DdmEngine:
         return x, r
 
     # -- parity / measurement taps
+    def fgmres_z(self, j: int) -> np.ndarray:
+        """Z_j = M(V_j) of the last FGMRES restart cycle (krylov.cpp:59-63)."""
+        z = np.empty(self.n, np.complex128)
+        self._check(self.lib.hddm_fgmres_z(self.h, j, C.c_void_p(z.ctypes.data), HDDM_HOST))
+        return z
+
     def window_dims(self) -> Tuple[int, int]:
         nx, ny = C.c_int(), C.c_int()
         self._check(self.lib.hddm_window_dims(self.h, C.byref(nx), C.byref(ny)))
