@@ -187,14 +187,7 @@ int hddm_solve_launches(const hddm_engine* e);
  * ||b - A x||/||b|| seen (refine's first pass, sparse.cpp:268-292) and how many
  * local solves exceeded the reference's 1e-11 correction threshold. */
 int hddm_refine_stats(const hddm_engine* e, double* max_local_relres, int* corrections);
-/* Dataflow-solve phase profile (libraries built with -DHDDM_DAG_PROF; zeros
- * otherwise): 8 task categories (sweep * 4 + unit kind * 2 + (M > 1)) x 8
- * counters (clock cycles of CTA phases 0..4, tasks at index 7). reset != 0
- * clears the counters after reading. hddm_solver_desc: the solver in use. */
-int hddm_dag_profile(hddm_engine* e, long long* out, int cap, int reset);
-/* Per-task trace of the last dataflow solve (profiling builds): 8 values per task
- * (start ns, end ns, SM, CTA, sweep, tile, unit, decomposition); cap in values. */
-int hddm_dag_trace(hddm_engine* e, long long* out, long long cap);
+/* The solver in use (descriptive). */
 const char* hddm_solver_desc(const hddm_engine* e);
 /* CUDA stream (cudaStream_t) the engine orders its work on. */
 void* hddm_stream(const hddm_engine* e);

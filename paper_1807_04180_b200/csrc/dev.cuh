@@ -8,32 +8,6 @@ namespace hddm {
 
 typedef double2 cplx;
 
-// diagonal block size of the dataflow solve's separators: L_ss is applied by
-// blocked substitution with these blocks inverted at factor time
-constexpr int kDiagBlk = 32;
-
-// A separator's diagonal block in the dataflow copies, cut in kDiagBlk panels b
-// (columns [b0, b1)): panel b holds the inverse Xinv_b of its diagonal block (unit
-// lower, strictly lower part) and the rows below it, L[b1 .. n, b0 .. b1).
-//   forward copy F, panels ascending:  [Xinv_b column-major | L below column-major]
-//   backward copy B, panels descending: [L below row-major | Xinv_b row-major]
-// so each sweep streams its panels front to back.
-__host__ __device__ __forceinline__ long long dpanel_size(int n, int b) {
-  const int b0 = b * kDiagBlk, b1 = (n < b0 + kDiagBlk) ? n : b0 + kDiagBlk, bw = b1 - b0;
-  return (long long)bw * (bw - 1) / 2 + (long long)bw * (n - b1);
-}
-__host__ __device__ __forceinline__ long long fpanel_off(int n, int b) {
-  long long o = 0;
-  for (int q = 0; q < b; ++q) o += dpanel_size(n, q);
-  return o;
-}
-__host__ __device__ __forceinline__ long long bpanel_off(int n, int b) {
-  long long o = 0;
-  const int nb = (n + kDiagBlk - 1) / kDiagBlk;
-  for (int q = nb - 1; q > b; --q) o += dpanel_size(n, q);
-  return o;
-}
-
 __host__ __device__ __forceinline__ cplx cmk(double r, double i) { return make_double2(r, i); }
 __host__ __device__ __forceinline__ cplx cadd(cplx a, cplx b) { return cmk(a.x + b.x, a.y + b.y); }
 __host__ __device__ __forceinline__ cplx csub(cplx a, cplx b) { return cmk(a.x - b.x, a.y - b.y); }

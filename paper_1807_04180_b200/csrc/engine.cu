@@ -25,7 +25,6 @@
 
 #include "hddm.h"
 #include "hddm_internal.h"
-#include "dag_plan.h"
 #include "kernels.cuh"
 #include "kernels_krylov.cuh"
 
@@ -338,19 +337,7 @@ struct hddm_engine {
     }
     return mask;
   }
-  int solve_launches() const { return dag ? 2 : solve_launch_count(plan); }
-  // dataflow solve (kernels_dag.cu; HDDM_SOLVER=level selects the level-synchronous one)
-  bool dag = false;
-  DagArgs dag_args0{};   // tables; per-call fields filled by enqueue_solve
-  int dag_ntile = 0;
-  DagSnV* d_dsn = nullptr;
-  cplx* d_vF = nullptr;
-  cplx* d_vB = nullptr;
-  long long dag_fwd_full = 0, dag_fwd_live = 0;  // forward values read per step (all tiles)
-  void build_dag();
-  std::string dag_desc;
-  std::vector<DagTask> dag_tasks_host;
-  std::vector<int> dag_units_host;  // per tile: its decomposition
+  int solve_launches() const { return solve_launch_count(plan); }
 };
 
 // ----------------------------------------------------------------- creation
@@ -513,14 +500,7 @@ void hddm_engine::create(const hddm_problem& p) {
     d_vstr = upload(h_vstr);
     d_cbase = upload(cb);
   }
-  {
-    const char* sv = std::getenv("HDDM_SOLVER");
-    dag = sv && std::string(sv) == "dag";  // experimental (measured slower)
-  }
-  if (dag)
-    build_dag();
-  else
-    build_plan();
+  build_plan();
   for (int k = 0; k < 3; ++k) {
     d_U[k] = dalloc<cplx>(size_t(nsub) * nw);
     d_Z[k] = dalloc<int>(nsub);
@@ -680,99 +660,6 @@ void hddm_engine::create(const hddm_problem& p) {
 
   factorize();
   run_probe();
-}
-
-// Dataflow solve plan (dag_plan.cu): member tiles of <= kDagMaxM members per class
-// (near-equal sizes), the unit decompositions and the task list, uploaded once.
-void hddm_engine::build_dag() {
-  std::vector<DagTileIn> tiles;
-  for (int c = 0; c < ncls; ++c) {
-    const int m = S.cls_ptr[c + 1] - S.cls_ptr[c];
-    const int nt = (m + kDagMaxM - 1) / kDagMaxM;
-    for (int ti = 0, k0 = 0; ti < nt; ++ti) {
-      const int M = m / nt + (ti < m % nt ? 1 : 0);
-      DagTileIn T{};
-      T.cb = (long long)S.cls_ptr[c] * nw + k0;
-      T.c = c;
-      T.m = m;
-      T.M = M;
-      for (int k = 0; k < kDagMaxM; ++k) T.t[k] = S.cls_members[S.cls_ptr[c] + k0 + std::min(k, M - 1)];
-      tiles.push_back(T);
-      k0 += M;
-    }
-  }
-  // supernodes whose subtree holds a transfer-patch node (the only nonzero RHS
-  // entries at steps >= 2; the others' forward results are exactly 0)
-  const std::vector<int> mask = patch_union_mask();
-  std::vector<char> live(Y.sn.size(), 0);
-  for (size_t s = 0; s < Y.sn.size(); ++s) {  // postorder
-    const SnNode& a = Y.sn[s];
-    char any = 0;
-    for (int i = 0; i < a.n && !any; ++i) any = mask[Y.perm[a.c0 + i]] != 0;
-    for (int c = 0; c < a.nch; ++c) any |= live[a.child[c]];
-    live[s] = any;
-  }
-  DagPlanHost P;
-  build_dag_plan(Y, live, tiles, P);
-  DagArgs& A = dag_args0;
-  A = DagArgs{};
-  A.sn = upload(P.sn);
-  A.row_first = upload(P.row_first);
-  A.row_dpos = upload(P.row_dpos);
-  A.row_boff = upload(P.row_boff);
-  A.col_off = upload(P.col_off);
-  for (size_t d = 0; d < P.dec.size(); ++d) {
-    const auto& D = P.dec[d];
-    DagDec& G = A.dec[d];
-    G.unit = upload(D.unit);
-    G.lv = upload(D.lv);
-    G.lvsn = upload(D.lvsn);
-    G.lsr = upload(D.lsr);
-    std::vector<int4> lrm(D.lrm.size() / 4);
-    for (size_t k = 0; k < lrm.size(); ++k)
-      lrm[k] = make_int4(D.lrm[4 * k], D.lrm[4 * k + 1], D.lrm[4 * k + 2], D.lrm[4 * k + 3]);
-    G.lrm = upload(lrm);
-    G.lrx = upload(D.lrx);
-    G.xe = upload(D.xe);
-    G.ch = upload(D.ch);
-    G.cmeta = upload(D.cmeta);
-    G.row_slot = upload(D.row_slot);
-    G.in_ptr = upload(D.in_ptr);
-    G.in_ref = upload(D.in_ref);
-    G.in_live = upload(D.in_live);
-    G.ext = upload(D.ext);
-    G.ext_src = upload(D.ext_src);
-    G.G = D.G;
-    G.hb = D.hb;
-  }
-  A.tile = upload(P.tile);
-  A.task = upload(P.task);
-  A.ntask = int(P.task.size());
-  A.ticket = dalloc<int>(1);
-  A.done = dalloc<int>(P.task.size());
-  A.P = dalloc<cplx>(std::max<long long>(P.nP, 1));
-  A.smem_bytes = int(P.smem_bytes);
-  A.prof = dalloc<long long>(64);
-  A.trace = dalloc<long long>(8 * P.task.size());
-  dag_tasks_host = P.task;
-  dag_units_host.clear();
-  for (const DagTile& T : P.tile) dag_units_host.push_back(T.dec);
-  CK(cudaMemsetAsync(A.prof, 0, 64 * sizeof(long long), st));
-  A.nvF = Y.nvF;
-  A.nvB = Y.nvB;
-  dag_ntile = int(P.tile.size());
-  dag_grid(A.smem_bytes);  // sets the kernel's shared-memory attribute (outside any capture)
-  // forward values read per step by all tiles: every unit at step 1, the live ones after
-  dag_fwd_full = dag_fwd_live = 0;
-  for (const DagTile& T : P.tile)
-    for (const DagUnit& U : P.dec[T.dec].unit) {
-      dag_fwd_full += U.f1 - U.f0;
-      if (U.live) dag_fwd_live += U.f1 - U.f0;
-    }
-  char buf[256];
-  std::snprintf(buf, sizeof buf, "dataflow solve: %d tiles, %d tasks, %lld KB smem/CTA, %d CTAs, %lld partial slots",
-                dag_ntile, A.ntask, P.smem_bytes / 1024, dag_grid(A.smem_bytes), P.nP);
-  dag_desc = buf;
 }
 
 // Solve plan: the ND tree level by level. Forward: leaves, then separator rows
@@ -1107,29 +994,7 @@ void hddm_engine::factorize() {
   int* d_ai = upload(aent_i);
   int* d_aj = upload(aent_j);
   int* d_ext = upload(Y.extadd);
-  if (dag) {
-    d_vF = dalloc<cplx>(size_t(ncls) * Y.nvF);
-    d_vB = dalloc<cplx>(size_t(ncls) * Y.nvB);
-  } else {
-    d_vals = dalloc<cplx>(size_t(ncls) * Y.nvals);
-  }
-  std::vector<DagSnV> dsn(Y.sn.size());
-  for (size_t s = 0; s < Y.sn.size(); ++s) {
-    const SnNode& a = Y.sn[s];
-    dsn[s] = {a.fdiag, a.frows, a.bdinv, a.bdiag, a.brows, a.rs0, a.nrs};
-  }
-  int* d_sf = nullptr;
-  int* d_sfr = nullptr;
-  long long* d_sbo = nullptr;
-  int* d_co = nullptr;
-  if (dag) {
-    d_dsn = upload(dsn);
-    d_sf = upload(Y.srow_first);
-    d_sfr = upload(Y.srow_front);
-    std::vector<long long> bo(Y.srow_boff.begin(), Y.srow_boff.end());
-    d_sbo = upload(bo);
-    d_co = upload(Y.col_off);
-  }
+  d_vals = dalloc<cplx>(size_t(ncls) * Y.nvals);
   int fmax = 0;
   for (const SnNode& a : Y.sn) fmax = std::max(fmax, a.n + int(a.rows.size()));
   if (size_t(2) * sizeof(cplx) * fmax > factor_smem_limit())
@@ -1139,9 +1004,7 @@ void hddm_engine::factorize() {
     d_lss = dalloc<cplx>(size_t(ncls) * nlss);
     d_lssc = dalloc<cplx>(size_t(ncls) * nlss);
   }
-  if (d_vals) CK(cudaMemsetAsync(d_vals, 0, size_t(ncls) * Y.nvals * sizeof(cplx), st));
-  if (d_vF) CK(cudaMemsetAsync(d_vF, 0, size_t(ncls) * Y.nvF * sizeof(cplx), st));
-  if (d_vB) CK(cudaMemsetAsync(d_vB, 0, size_t(ncls) * Y.nvB * sizeof(cplx), st));
+  CK(cudaMemsetAsync(d_vals, 0, size_t(ncls) * Y.nvals * sizeof(cplx), st));
   int* d_status = dalloc<int>(ncls);
   CK(cudaMemsetAsync(d_status, 0, sizeof(int) * ncls, st));
   // class batches bounded by ~8 GB of front workspace
@@ -1167,16 +1030,7 @@ void hddm_engine::factorize() {
     A.naent = naent;
     A.front = d_front;
     A.front_words = Y.front_words;
-    A.vals = d_vals ? d_vals + size_t(c0) * Y.nvals : nullptr;
-    A.vF = d_vF ? d_vF + size_t(c0) * Y.nvF : nullptr;
-    A.vB = d_vB ? d_vB + size_t(c0) * Y.nvB : nullptr;
-    A.nvF = Y.nvF;
-    A.nvB = Y.nvB;
-    A.dsn = d_dsn;
-    A.srow_first = d_sf;
-    A.srow_front = d_sfr;
-    A.srow_boff = d_sbo;
-    A.col_off = d_co;
+    A.vals = d_vals + size_t(c0) * Y.nvals;
     A.nvals = Y.nvals;
     A.lss = d_lss ? d_lss + size_t(c0) * nlss : nullptr;
     A.lssc = d_lssc ? d_lssc + size_t(c0) * nlss : nullptr;
@@ -1199,8 +1053,6 @@ void hddm_engine::factorize() {
   dfree(d_aj);
   dfree(d_ext);
   dfree(d_status);
-  for (void* p : {(void*)d_sf, (void*)d_sfr, (void*)d_sbo, (void*)d_co})
-    if (p) dfree(p);
   factor_ms = now_ms() - t0;
 }
 
@@ -1428,7 +1280,7 @@ void hddm_engine::enqueue_step_front(int s, cudaStream_t stream, unsigned long l
   if (!(sskip & 2)) launch_gather(A, stream);
   static const bool no_solve = std::getenv("HDDM_STEP_NOSOLVE") != nullptr;  // profiling aid
   SolveArgs SA = solve_args(d_B, A.Ucur, d_Y, A.zc, 0);
-  if (s >= 2 && (plan.has_sparse || dag)) {  // RHS nonzero only on the transfer patches
+  if (s >= 2 && plan.has_sparse) {  // RHS nonzero only on the transfer patches
     // skipped subtrees read as z = 0 in the backward (zval), so X need not be
     // cleared (HDDM_CLEAR_X: clear it anyway, A/B timing aid)
     static const bool clear_x = std::getenv("HDDM_CLEAR_X") != nullptr;
@@ -1453,19 +1305,6 @@ void hddm_engine::enqueue_step_front(int s, cudaStream_t stream, unsigned long l
 // level chain on its own forked stream (classes overlap; a class's vectors stay
 // L2-resident between its consecutive levels), joined afterwards.
 void hddm_engine::enqueue_solve(const SolveArgs& SA, cudaStream_t stream, const CheckArgs* check) {
-  if (dag) {
-    DagArgs A = dag_args0;
-    A.vF = d_vF;
-    A.vB = d_vB;
-    A.flag = SA.flag;
-    A.flag_on = SA.flag_on;
-    A.sparse = SA.sparse_rhs;
-    A.B = SA.B;
-    A.X = SA.X;
-    launch_dag_solve(A, dag_ntile, Y.nring, stream);
-    if (check) launch_check_partials(*check, stream);
-    return;
-  }
   const int nt = int(plan.groups.size());
   if (!per_class_streams || nt == 1 || (stream != st && stream != st2)) {
     for (int g = 0; g < nt; ++g) launch_solve_group(SA, plan, g, stream);
@@ -2163,45 +2002,13 @@ int hddm_stage_times(hddm_engine* e, double* ms, long long* count, int cap, int*
 
 long long hddm_launch_count(const hddm_engine* e) { return e->launches; }
 
-int hddm_dag_profile(hddm_engine* e, long long* out, int cap, int reset) {
-  return guarded(e, [&] {
-    if (!e->dag) throw ConfigErr("not the dataflow solver");
-    CK(cudaStreamSynchronize(e->st));
-    CK(cudaMemcpy(out, e->dag_args0.prof, sizeof(long long) * std::min(cap, 64), cudaMemcpyDeviceToHost));
-    if (reset) CK(cudaMemset(e->dag_args0.prof, 0, 64 * sizeof(long long)));
-  });
+const char* hddm_solver_desc(const hddm_engine* e) {
+  (void)e;
+  return "level-synchronous batched supernodal solve";
 }
-
-int hddm_dag_trace(hddm_engine* e, long long* out, long long cap) {
-  return guarded(e, [&] {
-    if (!e->dag) throw ConfigErr("not the dataflow solver");
-    CK(cudaStreamSynchronize(e->st));
-    const long long n = std::min<long long>(cap / 12, (long long)e->dag_tasks_host.size());
-    std::vector<long long> tr(8 * n);
-    CK(cudaMemcpy(tr.data(), e->dag_args0.trace, sizeof(long long) * 8 * n, cudaMemcpyDeviceToHost));
-    for (long long t = 0; t < n; ++t) {  // (start, end, sm, cta, kind, tile, unit, dec, phase 1..4 cycles)
-      const DagTask& T = e->dag_tasks_host[t];
-      for (int q = 0; q < 4; ++q) out[12 * t + q] = tr[8 * t + q];
-      out[12 * t + 4] = T.kind;
-      out[12 * t + 5] = T.tile;
-      out[12 * t + 6] = T.unit;
-      out[12 * t + 7] = e->dag_units_host[T.tile];
-      for (int q = 0; q < 4; ++q) out[12 * t + 8 + q] = tr[8 * t + 4 + q];
-    }
-  });
-}
-
-const char* hddm_solver_desc(const hddm_engine* e) { return e->dag ? e->dag_desc.c_str() : "level-synchronous"; }
 
 int hddm_fwd_entries(const hddm_engine* e, long long* full, long long* sparse_rhs) {
   if (!e || !full || !sparse_rhs) return 1;
-  if (e->dag) {  // per class; the steady-state share from the live units of every tile
-    *full = e->Y.nvF;
-    *sparse_rhs = e->dag_fwd_full > 0 ? (long long)(double(e->Y.nvF) * double(e->dag_fwd_live) /
-                                                    double(e->dag_fwd_full))
-                                      : *full;
-    return 0;
-  }
   *full = e->fwd_entries_full ? e->fwd_entries_full : e->Y.nnz_stored;
   *sparse_rhs = e->plan.has_sparse ? e->fwd_entries_sparse : *full;
   return 0;
@@ -2225,7 +2032,7 @@ int hddm_time_solve(hddm_engine* e, int reps, double* ms_per_solve) {
     SolveArgs SA = e->solve_args(e->d_B, e->d_C, e->d_Y, e->d_zero, on);
     // HDDM_TIME_SPARSE: the steady-state (steps >= 2) forward plan; B then holds the last
     // step's right-hand sides, which are nonzero only on the transfer patches
-    if (std::getenv("HDDM_TIME_SPARSE") && (e->plan.has_sparse || e->dag)) SA.sparse_rhs = 1;
+    if (std::getenv("HDDM_TIME_SPARSE") && e->plan.has_sparse) SA.sparse_rhs = 1;
     e->enqueue_solve(SA, st);
     set_solve_skip(0, -1);
     CK(cudaStreamEndCapture(st, &g));

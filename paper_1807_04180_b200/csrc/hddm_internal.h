@@ -38,14 +38,6 @@ struct SnNode {
   int drow0 = 0;             // leaf: first row-table entry of its band rows
   long front_off = 0;        // workspace offset of the (n+rows) x (n+rows) front
   int nextadd = 0, extadd0 = 0;  // index maps for the children's update blocks
-  // dataflow-solve layout (two copies of the factor, one per sweep):
-  //   forward copy  F: [diag | rows]  separators: L_ss column-major packed with its
-  //                    kDiagBlk diagonal blocks inverted; leaves: band; rows column-major
-  //   backward copy B: [1/D | diag | rows]  diag row-major packed (blocks inverted) or
-  //                    band; rows row-major (each row [first, n))
-  int rs0 = 0, nrs = 0;      // block rows sorted by first column: S.srow_*[rs0 .. rs0+nrs)
-  long fdiag = 0, frows = 0, fend = 0;           // offsets in F (per class)
-  long bdinv = 0, bdiag = 0, brows = 0, bend = 0;  // offsets in B (per class)
 };
 
 // Rows [r0, r0+nr) (relative to dst.c0) of ancestor `dst` against the columns of
@@ -83,15 +75,7 @@ struct Symbolic {
   std::vector<int> aent0;            // size sn+1
   std::vector<int> aent_i, aent_j;   // front indices
   std::vector<int> aent_node, aent_kind;  // window node, 0 diag 1 W 2 E 3 S 4 N
-  // dataflow layout (see SnNode): per sorted block row -- first column, destination
-  // position, row index in the owner's front, offset of entry [first] relative to
-  // brows; per position: offset of its column relative to frows (column-major rows)
-  std::vector<int> srow_first, srow_dpos, srow_front;
-  std::vector<long> srow_boff;
-  std::vector<int> col_off;   // per position p of supernode s: start of column p - c0
-  long nvF = 0, nvB = 0;      // values per class in F and B
 };
-
 
 void build_symbolic(int nx, int ny, Symbolic& S);
 std::vector<int> nd_order(int nx, int ny);

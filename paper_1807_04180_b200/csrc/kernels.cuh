@@ -107,11 +107,6 @@ struct SolvePlan {
   // off by default, HDDM_CTA_RUN / HDDM_CTA_DIAG)
 };
 
-// dataflow solve (kernels_dag.cu): ring rows, then the persistent task kernel
-struct DagArgs;
-void launch_dag_solve(const DagArgs& A, int ntile, int nring, cudaStream_t st);
-int dag_grid(int smem_bytes);  // CTAs of the persistent grid (sets the smem attribute)
-
 // one tile group's full solve (all levels) on one stream
 void launch_solve_group(const SolveArgs& A, const SolvePlan& P, int g, cudaStream_t st);
 int solve_launch_count(const SolvePlan& P);  // kernels of one solve over all tiles
@@ -122,12 +117,6 @@ void set_solve_pdl(bool on);                  // programmatic dependent launch o
 void set_fwd_shape(int which, int level, int E);
 
 // ------------------------------------------------------------------ factor
-// per supernode offsets of the dataflow layout (SnNode, hddm_internal.h)
-struct DagSnV {
-  long long fdiag, frows, bdinv, bdiag, brows;
-  int rs0, nrs;
-};
-
 struct FactorArgs {
   const DevSn* sn;
   const DevBlk* blk;
@@ -148,15 +137,6 @@ struct FactorArgs {
   const long long* lss_off;  // per supernode: offset of its block, -1: applied as an inverse
   long long nlss;
   int* status;        // per class: 0 ok, 1 zero pivot
-  // dataflow layout (vF != null: emit the two copies instead of vals)
-  cplx* vF;
-  cplx* vB;
-  long long nvF, nvB;
-  const DagSnV* dsn;
-  const int* srow_first;
-  const int* srow_front;
-  const long long* srow_boff;
-  const int* col_off;
 };
 
 // fmax: largest front (own columns + update rows); the shared scratch is sized from it

@@ -17,7 +17,6 @@
 #include <algorithm>
 
 #include "dev.cuh"
-#include "hddm_internal.h"
 #include "kernels.cuh"
 
 namespace hddm {
@@ -85,68 +84,6 @@ __global__ void __launch_bounds__(512) k_factor_node(FactorArgs A, const int* no
       }
     }
     __syncthreads();
-  }
-  if (A.vF) {  // dataflow layout: forward copy F, backward copy B
-    const DagSnV d = A.dsn[s];
-    cplx* VF = A.vF + (long long)c * A.nvF;
-    cplx* VB = A.vB + (long long)c * A.nvB;
-    for (int j = tid; j < n; j += nt) VB[d.bdinv + j] = cdiv(cmk(1.0, 0.0), F[(long long)j * Fn + j]);
-    if (sn.kind == 1) {
-      // the inverse X_b of each kDiagBlk diagonal block (unit lower):
-      // X[i][j] = -(L[i][j] + sum_{j<q<i} L[i][q] X[q][j]), a thread per column, kept
-      // in the front's (unused) upper triangle X[i][j] -> F[j][i]; then the panels
-      for (int j = tid; j < n; j += nt) {
-        const int b1 = min(n, (j / kDiagBlk + 1) * kDiagBlk);
-        for (int i = j + 1; i < b1; ++i) {
-          const cplx* Li = F + (long long)i * Fn;
-          cplx acc = Li[j];
-          for (int q = j + 1; q < i; ++q) cfma(acc, Li[q], F[(long long)j * Fn + q]);
-          F[(long long)j * Fn + i] = cmk(-acc.x, -acc.y);
-        }
-      }
-      __syncthreads();
-      const int nb = (n + kDiagBlk - 1) / kDiagBlk;
-      for (int b = 0; b < nb; ++b) {
-        const int b0 = b * kDiagBlk, b1 = min(n, b0 + kDiagBlk), bw = b1 - b0;
-        cplx* Fp = VF + d.fdiag + fpanel_off(n, b);
-        cplx* Bp = VB + d.bdiag + bpanel_off(n, b);
-        const long long xs = (long long)bw * (bw - 1) / 2, ls = (long long)bw * (n - b1);
-        for (int jj = warp; jj < bw; jj += nwarp) {
-          const int j = b0 + jj;
-          for (int ii = jj + 1 + lane; ii < bw; ii += 32) {  // X part
-            const cplx v = F[(long long)j * Fn + (b0 + ii)];
-            Fp[(long long)jj * (bw - 1) - (long long)jj * (jj - 1) / 2 + (ii - jj - 1)] = v;
-            Bp[ls + (long long)ii * (ii - 1) / 2 + jj] = v;
-          }
-          for (int i = b1 + lane; i < n; i += 32) {  // L below
-            const cplx v = F[(long long)i * Fn + j];
-            Fp[xs + (long long)jj * (n - b1) + (i - b1)] = v;
-            Bp[(long long)(i - b1) * bw + jj] = v;
-          }
-        }
-      }
-    } else {
-      for (int i = warp; i < n; i += nwarp) {
-        const int first = A.row_first[sn.drow0 + i];
-        const long long o = A.row_off[sn.drow0 + i] - sn.diag_off - first;
-        for (int q = first + lane; q < i; q += 32) {
-          const cplx v = F[(long long)i * Fn + q];
-          VB[d.bdiag + o + q] = v;
-          VF[d.fdiag + o + q] = v;
-        }
-      }
-    }
-    for (int r = warp; r < d.nrs; r += nwarp) {
-      const int first = A.srow_first[d.rs0 + r];
-      const cplx* src = F + (long long)A.srow_front[d.rs0 + r] * Fn;
-      cplx* dstB = VB + d.brows + A.srow_boff[d.rs0 + r] - first;
-      for (int j = first + lane; j < n; j += 32) {
-        const cplx v = src[j];
-        dstB[j] = v;
-        VF[d.frows + A.col_off[sn.c0 + j] + r] = v;
-      }
-    }
-    return;
   }
   // emit 1/D
   for (int j = tid; j < n; j += nt)

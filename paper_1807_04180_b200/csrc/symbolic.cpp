@@ -333,63 +333,6 @@ void build_symbolic(int nx, int ny, Symbolic& S) {
   }
   S.aent0[nsn] = int(S.aent_i.size());
 
-  // dataflow layout: per supernode (postorder) a contiguous range in each copy
-  S.srow_first.clear();
-  S.srow_dpos.clear();
-  S.srow_front.clear();
-  S.srow_boff.clear();
-  S.col_off.assign(n, 0);
-  long fo = 0, bo = 0;
-  for (int s = 0; s < nsn; ++s) {
-    SnNode& nd = S.sn[s];
-    // rows of the blocks, empty padding rows dropped, sorted by first column
-    struct R {
-      int first, dpos, front;
-    };
-    std::vector<R> rows;
-    for (int b = nd.blk0; b < nd.blk0 + nd.nblk; ++b) {
-      const Block& B = S.blk[b];
-      for (int r = 0; r < B.nr; ++r) {
-        const int f = S.row_first[B.row0 + r];
-        if (f >= nd.n) continue;
-        rows.push_back({f, S.sn[B.dst].c0 + B.r0 + r, B.front0 + r});
-      }
-    }
-    std::stable_sort(rows.begin(), rows.end(), [](const R& a, const R& b) { return a.first < b.first; });
-    nd.rs0 = int(S.srow_first.size());
-    nd.nrs = int(rows.size());
-    long roff = 0;
-    for (const R& r : rows) {
-      S.srow_first.push_back(r.first);
-      S.srow_dpos.push_back(r.dpos);
-      S.srow_front.push_back(r.front);
-      S.srow_boff.push_back(roff);
-      roff += nd.n - r.first;
-    }
-    long band = 0;
-    if (nd.kind == 0)
-      for (int i = 0; i < nd.n; ++i) band += i - S.row_first[nd.drow0 + i];
-    const long diag = nd.kind == 1 ? long(nd.n) * (nd.n - 1) / 2 : band;
-    nd.fdiag = fo;
-    nd.frows = fo + diag;
-    // column-major rows: column q holds the rows with first <= q (a prefix)
-    long co = 0;
-    size_t cnt = 0;
-    for (int q = 0; q < nd.n; ++q) {
-      while (cnt < rows.size() && rows[cnt].first <= q) ++cnt;
-      S.col_off[nd.c0 + q] = int(co);
-      co += long(cnt);
-    }
-    nd.fend = nd.frows + co;
-    fo = nd.fend;
-    nd.bdinv = bo;
-    nd.bdiag = bo + nd.n;
-    nd.brows = nd.bdiag + diag;
-    nd.bend = nd.brows + roff;
-    bo = nd.bend;
-  }
-  S.nvF = fo;
-  S.nvB = bo;
 }
 
 }  // namespace hddm

@@ -106,7 +106,7 @@ class FgmresResult:
 
 
 _lib = None
-_OPTIONAL = {"hddm_fgmres_z", "hddm_dag_profile", "hddm_solver_desc", "hddm_dag_trace"}
+_OPTIONAL = {"hddm_fgmres_z", "hddm_solver_desc"}
 
 
 def load_library(path: str = LIB_PATH):
@@ -153,9 +153,7 @@ def load_library(path: str = LIB_PATH):
         "hddm_solve_launches": (C.c_int, [vp]),
         "hddm_stage_name": (C.c_char_p, [C.c_int]),
         "hddm_stream": (vp, [vp]),
-        "hddm_dag_profile": (C.c_int, [vp, P(C.c_longlong), C.c_int, C.c_int]),
         "hddm_solver_desc": (C.c_char_p, [vp]),
-        "hddm_dag_trace": (C.c_int, [vp, P(C.c_longlong), C.c_longlong]),
     }
     for name, (res, args) in sigs.items():
         if name in _OPTIONAL and not hasattr(lib, name):
@@ -453,22 +451,6 @@ class DdmEngine:
 
     def launch_count(self) -> int:
         return int(self.lib.hddm_launch_count(self.h))
-
-    def dag_profile(self, reset: bool = True):
-        """Phase cycles of the dataflow solve (profiling builds): {category: [ph0..ph4, tasks]}."""
-        buf = np.zeros(64, np.int64)
-        self._check(self.lib.hddm_dag_profile(self.h, buf.ctypes.data_as(C.POINTER(C.c_longlong)),
-                                              64, 1 if reset else 0))
-        names = ["fwd_subtree_M1", "fwd_subtree_Mn", "fwd_single_M1", "fwd_single_Mn",
-                 "bwd_subtree_M1", "bwd_subtree_Mn", "bwd_single_M1", "bwd_single_Mn"]
-        return {names[c]: [int(x) for x in buf[8 * c: 8 * c + 6]] + [int(buf[8 * c + 7])]
-                for c in range(8)}
-
-    def dag_trace(self, ntask: int = 1 << 20):
-        """Per-task (start ns, end ns, SM, CTA, sweep, tile, unit, dec) of the last dataflow solve."""
-        buf = np.zeros(12 * ntask, np.int64)
-        self._check(self.lib.hddm_dag_trace(self.h, buf.ctypes.data_as(C.POINTER(C.c_longlong)), len(buf)))
-        return buf.reshape(-1, 12)
 
     def solver_desc(self) -> str:
         return self.lib.hddm_solver_desc(self.h).decode()
