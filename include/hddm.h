@@ -61,6 +61,11 @@ typedef struct hddm_problem_s {
   int threads; /* accepted for DdmConfig parity; unused (the GPU replaces WorkerPool) */
   double lens_amp, lens_xc, lens_yc, lens_w;
   int device; /* CUDA device ordinal */
+  /* MediumModel::interior and ::margin (medium.hpp:23-24) when has_box != 0; else
+   * the grid's interior box and (n_ext + 1) h, as make_setup sets them
+   * (config.cpp:175-223). The margin is raised to (n_ext + 1) h (ddm.cpp:66-67). */
+  int has_box;
+  double box_x0, box_x1, box_y0, box_y1, margin;
 } hddm_problem;
 
 /* DdmStats (ddm.hpp:30-39) without the history vector (returned separately). */

@@ -1812,7 +1812,9 @@ int hddm_fgmres(hddm_engine* e, const double* b, double* x, double tol, int max_
     int mcap = restart > 0 ? restart : max_iters;
     if (mcap < 1) mcap = 1;
     e->ensure_krylov(mcap);
-    const int ld = mcap + 1;  // H column j: d_H[j*ld + i]
+    // the workspace (and the cycle graph) may be wider than this call needs: H column j
+    // is d_H[j*ld + i] with the workspace's leading dimension
+    const int ld = e->kry_m + 1;
     cudaStream_t st = e->st;
     CK(cudaMemcpyAsync(e->d_b, b, n * sizeof(cplx),
                        memkind == HDDM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
@@ -1857,7 +1859,7 @@ int hddm_fgmres(hddm_engine* e, const double* b, double* x, double tol, int max_
         CK(cudaMemcpyAsync(e->d_scal + 8, e->h_scal + 8, sizeof(double), cudaMemcpyHostToDevice, st));
         launch_scale_div(e->V[0], e->d_r, e->d_scal + 8, n, st);
         launch_init_g(e->d_g, m, e->d_scal + 8, st);
-        CK(cudaMemsetAsync(e->d_H, 0, sizeof(cplx) * size_t(mcap) * ld, st));
+        CK(cudaMemsetAsync(e->d_H, 0, sizeof(cplx) * size_t(e->kry_m) * ld, st));
         ks.j = 0;
         ks.m = m;
         ks.k = 0;

@@ -153,6 +153,13 @@ int build_setup(const hddm_problem& p, Setup& S, std::string& msg) {
   m.by0 = S.y0;
   m.by1 = S.y0 + S.my * S.h;
   m.margin = (S.ext + 1) * S.h;  // ddm.cpp:66-67
+  if (p.has_box) {  // the caller's MediumModel::interior / margin (medium.hpp:23-24)
+    m.bx0 = p.box_x0;
+    m.bx1 = p.box_x1;
+    m.by0 = p.box_y0;
+    m.by1 = p.box_y1;
+    m.margin = std::max(p.margin, m.margin);
+  }
   m.lamp = p.lens_amp;
   m.lxc = p.lens_xc;
   m.lyc = p.lens_yc;

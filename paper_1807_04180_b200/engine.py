@@ -51,6 +51,8 @@ class _Problem(C.Structure):
         ("c_sigma", C.c_double), ("sigma0", C.c_double), ("threads", C.c_int),
         ("lens_amp", C.c_double), ("lens_xc", C.c_double), ("lens_yc", C.c_double),
         ("lens_w", C.c_double), ("device", C.c_int),
+        ("has_box", C.c_int), ("box_x0", C.c_double), ("box_x1", C.c_double),
+        ("box_y0", C.c_double), ("box_y1", C.c_double), ("margin", C.c_double),
     ]
 
 

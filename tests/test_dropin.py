@@ -1,0 +1,93 @@
+"""Drop-in boundary: the reference's OWN command line and unit tests, compiled
+unchanged against include/helmddm_b200/dropin/helmddm/ddm.hpp with
+paper_1807_04180_b200/dropin/ddm_b200.cpp in place of src/ddm.cpp and linked to
+libhddm.so (oracle/Makefile `dropin`).
+
+CPU: the binaries build (where /root/reference exists) and link libhddm.so.
+GPU: the reference's test_ddm.cpp / test_cli.cpp test cases pass on the GPU engine,
+and `helmddm solve` of the drop-in build reproduces the unmodified reference CLI's
+field and statistics on the same config files."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, rel_l2
+
+REF = os.path.join(ROOT, "oracle", "_ref")
+CLI_GPU = os.path.join(REF, "helmddm_gpu")
+UNITS_GPU = os.path.join(REF, "ref_units_gpu")
+CLI_REF = os.path.join(REF, "helmddm")
+
+
+def _build():
+    if os.path.isdir("/root/reference/proj/src"):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "dropin", "ref-cli"], check=True)
+
+
+def test_dropin_binaries_build_and_link():
+    _build()
+    for exe in (CLI_GPU, UNITS_GPU):
+        assert os.path.exists(exe), exe
+        out = subprocess.run(["ldd", exe], capture_output=True, text=True).stdout
+        assert "libhddm.so" in out and "not found" not in out, out
+
+
+def test_dropin_cli_usage_runs_without_gpu():
+    _build()
+    out = subprocess.run([CLI_GPU], capture_output=True, text=True, timeout=60)
+    assert "usage: helmddm" in out.stdout + out.stderr
+
+
+@pytest.mark.gpu
+def test_reference_unit_tests_pass_on_gpu_engine(tmp_path):
+    """proj/tests/test_ddm.cpp (single window = direct solve, zero source, one ring per
+    sweep, congruent classes, four-window split, stopping rules, thread-count
+    independence, global apply, preconditioner scaling) and proj/tests/test_cli.cpp
+    (artifacts, fgmres solve-count identity, render byte-for-byte, exit codes, the
+    convergence study), unmodified."""
+    env = dict(os.environ, TMPDIR=str(tmp_path))
+    out = subprocess.run([UNITS_GPU], capture_output=True, text=True, timeout=1800, env=env, cwd=tmp_path)
+    assert out.returncode == 0, out.stdout[-4000:] + out.stderr[-2000:]
+    assert "| 0 failed" in out.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["ddm", "fgmres"])
+def test_dropin_cli_matches_reference_cli(tmp_path, mode):
+    """`helmddm solve` of the drop-in build vs the unmodified reference CLI, same config:
+    exit code, stats keys and counts, and the written field (HDMF) to 1e-8."""
+    if not os.path.exists(CLI_REF):
+        pytest.skip("reference CLI not built")
+    cfg_text = ("freq = 6\ngrid.ppw = 10\npart.n1 = 3\npart.n2 = 2\npml.n_overlap = 4\n"
+                "pml.n_ramp = 8\nsolver.tol = 1e-9\nsolver.max_steps = 60\nthreads = 2\n"
+                f"solver.mode = {mode}\nkrylov.tol = 1e-9\nkrylov.restart = 20\n")
+    res = {}
+    for tag, exe in (("ref", CLI_REF), ("gpu", CLI_GPU)):
+        d = tmp_path / tag
+        d.mkdir()
+        (d / "run.cfg").write_text(cfg_text + f"output.prefix = {d / 'out'}\n")
+        out = subprocess.run([exe, "solve", str(d / "run.cfg"), "--quiet"], capture_output=True,
+                             text=True, timeout=900, cwd=d)
+        stats = {}
+        for line in (d / "out_stats.txt").read_text().splitlines():
+            if " = " in line:
+                k, v = line.split(" = ", 1)
+                stats[k.strip()] = v.strip()
+        field = sorted(p for p in os.listdir(d) if p.endswith(".hdmf"))
+        res[tag] = (out.returncode, stats, [(d / p).read_bytes() for p in field])
+    assert res["gpu"][0] == res["ref"][0] == 0
+    sr, sg = res["ref"][1], res["gpu"][1]
+    assert set(sr) == set(sg)
+    for k in ("mode", "grid.cells", "grid.h", "partition", "pml.sigma0", "factor.classes",
+              "factor.backend.ldlt", "n_DDM_Iter", "n_GMRES_Iter", "n_Local_Solv", "converged"):
+        assert sr[k] == sg[k], (k, sr[k], sg[k])
+    assert len(res["ref"][2]) == len(res["gpu"][2]) >= 1
+    for br, bg in zip(res["ref"][2], res["gpu"][2]):
+        # HDMF (io.cpp:26-41): 40-byte header (magic, version, nx, ny, x0, y0, h)
+        # identical, complex payload within 1e-8 relative
+        assert len(br) == len(bg) and br[:40] == bg[:40]
+        fr = np.frombuffer(br[40:], dtype=np.complex128)
+        fg = np.frombuffer(bg[40:], dtype=np.complex128)
+        assert rel_l2(fg, fr) <= 1e-8
