@@ -186,9 +186,10 @@ def run_reference(args, world, rank):
         return
     prob = config(args.config)
     threads = os.cpu_count() or 1
-    # bounded sample: the reference needs ~1.6 s per config-4 sweep on 8 cores
+    # bounded sample: the reference needs ~0.6 s per config-4 sweep on 16 cores; the
+    # same warm-up count as the GPU arm
     steps = args.steps
-    warm = min(args.warmup, 1)
+    warm = args.warmup
     val, kind, thr, dt = reference_sample(prob, steps, warm, threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
@@ -242,6 +243,8 @@ def run_ours(args, world, rank, local):
     # dominant kernel group: the batched solve stage, timed on the engine stream
     # (CUDA graph of its kernels, right-hand sides of the last timed sweep)
     solve_ms_per = eng.time_solve(max(5, args.steps))
+    # the other step stages, each timed alone on the last sweep's state (CUDA events)
+    stage_ms = {k: eng.time_kernel(k, 20) for k in ("transfer", "check", "accumulate")}
     ms_max = allreduce_max(ms, world)
     value = world * args.steps / (ms_max / 1e3)
 
@@ -252,6 +255,17 @@ def run_ours(args, world, rank, local):
     achieved = B["B_solve"] / (solve_ms_per / 1e3) / 1e9 if solve_ms_per > 0 else None
     # steps >= 2 read only the forward factor blocks of patch-holding subtrees
     # (RHS nonzero on the transfer patches only); SURVEY 8(d) counts the blocks read
+    nw = prob.window[0] * prob.window[1]
+    stage_bytes = {"transfer": B["B_xfer"], "accumulate": B["B_acc"],
+                   "check": 16.0 * prob.nsub * nw}
+    stage_roof = {k: {"ms": stage_ms[k], "bytes": stage_bytes[k],
+                      "achieved_gbs": stage_bytes[k] / (stage_ms[k] / 1e3) / 1e9,
+                      "frac": stage_bytes[k] / (stage_ms[k] / 1e3) / 1e9 / peak}
+                  for k in stage_ms}
+    stage_roof["note"] = ("algorithmic bytes (SURVEY 8(d)): transfer B_xfer = 16(|patch|+|w|) per "
+                          "executed transfer, accumulate B_acc = 48|region| per subdomain, check "
+                          "= the solutions read once (16 n_w per subdomain; its reads of B on the "
+                          "transfer patches not counted: a lower bound)")
     fwd_full, fwd_sparse = eng.fwd_entries()
     saved = 16.0 * len(ci) * (fwd_full - fwd_sparse) * (args.steps - 1) / args.steps
     B_step_read = B["B_step"] - saved
@@ -294,11 +308,16 @@ def run_ours(args, world, rank, local):
     cpu = None
     if rank == 0 and not args.skip_cpu:
         try:
+            # the reference on every host core (the headline baseline) and on one core
+            # (SURVEY 8(d)); thread scaling is capped by its per-class mutex
             cval, kind, thr, dt = reference_sample(prob, args.cpu_steps, 0,
                                                    os.cpu_count() or 1)
+            cval1, _, thr1, dt1 = reference_sample(prob, 1, 0, 1)
             cpu = {"value": cval, "unit": UNIT, "cores": thr, "kind": kind,
                    "sample": f"precondition(r, K={args.cpu_steps}) on {prob.name}, dense "
-                             f"seeded r, {dt:.1f} s"}
+                             f"seeded r, {dt:.1f} s",
+                   "single_thread": {"value": cval1, "unit": UNIT, "cores": thr1,
+                                     "sample": f"precondition(r, K=1), {dt1:.1f} s"}}
         except Exception as exc:  # reported, not fatal
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
                    "sample": f"{type(exc).__name__}: {exc}"}
@@ -339,6 +358,7 @@ def run_ours(args, world, rank, local):
                               "bytes_per_step_full": B["B_step"],
                               "fwd_entries": {"full": fwd_full, "sparse_rhs": fwd_sparse},
                               "frac": step_achieved / peak, "all_active": all_active},
+            "stage_rooflines": stage_roof,
             "factor": factor_info,
             "solve_launches_per_step": eng.solve_launches(),
             "refine": {"max_first_pass_relres": max_local_rel,

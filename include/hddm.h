@@ -188,6 +188,11 @@ int hddm_time_solve(hddm_engine* e, int reps, double* ms_per_solve);
  * rows; E = 0 restores the heuristic. Drops the cached step graphs. Process-wide. */
 int hddm_tune_fwd_shape(hddm_engine* e, int which, int level, int E);
 int hddm_solve_launches(const hddm_engine* e);
+/* Device time of one launch of a step stage kernel on the state of the last sweep
+ * (>= 3 steps): which = 0 the 8-direction source transfer (k_rhs_transfer),
+ * 1 the per-subdomain residual check (k_check), 2 the blend-accumulate (into scratch).
+ * CUDA events on the engine stream, averaged over reps launches. */
+int hddm_time_kernel(hddm_engine* e, int which, int reps, double* ms_per_launch);
 /* Refinement diagnostics of the last call: the largest local-solve residual
  * ||b - A x||/||b|| seen (refine's first pass, sparse.cpp:268-292) and how many
  * local solves exceeded the reference's 1e-11 correction threshold. */

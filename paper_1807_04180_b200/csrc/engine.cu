@@ -368,8 +368,6 @@ void hddm_engine::create(const hddm_problem& p) {
   ng = (long long)S.gnx * S.gny;
   for (int c = 0; c < ncls; ++c)
     max_members = std::max(max_members, S.cls_ptr[c + 1] - S.cls_ptr[c]);
-  if (max_members > 256)  // the residual check assigns one member per thread
-    throw ConfigErr("a factor class with more than 256 subdomains is not supported");
   build_symbolic(wnx, wny, Y);
 
   // ---- symbolic tables
@@ -1275,10 +1273,10 @@ RefineArgs hddm_engine::refine_args(const cplx* Bp, cplx* X, const int* zc,
 void hddm_engine::enqueue_step_front(int s, cudaStream_t stream, unsigned long long cond) {
   const StepArgs A = step_args(s, d_f);
   // HDDM_STEP_SKIP (profiling aid, results invalid): 1 flags, 2 gather, 4 check, 8 accumulate
-  static const int sskip = std::getenv("HDDM_STEP_SKIP") ? std::atoi(std::getenv("HDDM_STEP_SKIP")) : 0;
+  static const int sskip = profiling_env("HDDM_STEP_SKIP") ? std::atoi(profiling_env("HDDM_STEP_SKIP")) : 0;
   if (!(sskip & 1)) launch_flags(A, ncls, stream);
   if (!(sskip & 2)) launch_gather(A, stream);
-  static const bool no_solve = std::getenv("HDDM_STEP_NOSOLVE") != nullptr;  // profiling aid
+  static const bool no_solve = profiling_env("HDDM_STEP_NOSOLVE") != nullptr;  // profiling aid
   SolveArgs SA = solve_args(d_B, A.Ucur, d_Y, A.zc, 0);
   if (s >= 2 && plan.has_sparse) {  // RHS nonzero only on the transfer patches
     // skipped subtrees read as z = 0 in the backward (zval), so X need not be
@@ -2023,14 +2021,14 @@ int hddm_time_solve(hddm_engine* e, int reps, double* ms_per_solve) {
     cudaStream_t st = e->st;
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    set_solve_skip(std::getenv("HDDM_SKIP") ? std::atoi(std::getenv("HDDM_SKIP")) : 0,
-                   std::getenv("HDDM_ONLY_TILE")
-                       ? std::atoi(std::getenv("HDDM_ONLY_TILE"))
-                       : (std::getenv("HDDM_ONLY_M") ? -2 - std::atoi(std::getenv("HDDM_ONLY_M")) : -1));
+    set_solve_skip(profiling_env("HDDM_SKIP") ? std::atoi(profiling_env("HDDM_SKIP")) : 0,
+                   profiling_env("HDDM_ONLY_TILE")
+                       ? std::atoi(profiling_env("HDDM_ONLY_TILE"))
+                       : (profiling_env("HDDM_ONLY_M") ? -2 - std::atoi(profiling_env("HDDM_ONLY_M")) : -1));
     // HDDM_ONLY_M=M: only the tile groups of M members (profiling aid)
     // HDDM_TIME_EMPTY: no RHS active -- every kernel exits after its setup, so
     // the time is the launch / dependency floor of the solve graph (profiling aid)
-    const int on = std::getenv("HDDM_TIME_EMPTY") ? 1 : 0;
+    const int on = profiling_env("HDDM_TIME_EMPTY") ? 1 : 0;
     SolveArgs SA = e->solve_args(e->d_B, e->d_C, e->d_Y, e->d_zero, on);
     // HDDM_TIME_SPARSE: the steady-state (steps >= 2) forward plan; B then holds the last
     // step's right-hand sides, which are nonzero only on the transfer patches
@@ -2043,7 +2041,7 @@ int hddm_time_solve(hddm_engine* e, int reps, double* ms_per_solve) {
     // HDDM_TIME_PAIR (profiling aid, results invalid): two instances run
     // concurrently on two streams; the time per solve then shows how much idle
     // capacity the single solve graph leaves
-    const bool pair = std::getenv("HDDM_TIME_PAIR") != nullptr;
+    const bool pair = profiling_env("HDDM_TIME_PAIR") != nullptr;
     if (pair) CK(cudaGraphInstantiate(&x2, g, 0));
     CK(cudaGraphDestroy(g));
     CK(cudaGraphLaunch(x, st));  // warm-up
@@ -2078,6 +2076,40 @@ int hddm_time_solve(hddm_engine* e, int reps, double* ms_per_solve) {
 }
 
 int hddm_solve_launches(const hddm_engine* e) { return solve_launch_count(e->plan); }
+
+int hddm_time_kernel(hddm_engine* e, int which, int reps, double* ms_per_launch) {
+  return guarded(e, [&] {
+    if (e->last_step < 3) throw ConfigErr("time_kernel needs a sweep sequence of at least 3 steps");
+    if (which < 0 || which > 2) throw ConfigErr("time_kernel: 0 transfer, 1 residual check, 2 accumulate");
+    // the state of the last step: its transfer (idempotent: rewrites the same patch
+    // values), its residual check (writes scratch partials), its blend-accumulate into
+    // a scratch field
+    StepArgs A = e->step_args(e->last_step, e->d_f);
+    A.asmb = e->d_tmp;
+    const CheckArgs Cc = e->check_args(e->d_B, A.Ucur, A.zc, nullptr, true);
+    auto run = [&] {
+      if (which == 0)
+        launch_transfer(A, e->st);
+      else if (which == 1)
+        launch_check_partials(Cc, e->st);
+      else
+        launch_accumulate(A, e->st);
+    };
+    run();
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a, e->st));
+    for (int r = 0; r < std::max(reps, 1); ++r) run();
+    CK(cudaEventRecord(b, e->st));
+    CK(cudaEventSynchronize(b));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    *ms_per_launch = ms / std::max(reps, 1);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  });
+}
 
 int hddm_tune_fwd_shape(hddm_engine* e, int which, int level, int E) {
   return guarded(e, [&] {

@@ -10,12 +10,27 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
 #include "hddm.h"
 
 namespace hddm {
+
+// Profiling knobs that change what the engine computes (leaving kernel families or
+// stages out, timing aids): read only in builds compiled with -DHDDM_PROFILING
+// (make EXTRA=-DHDDM_PROFILING); in the product library they are ignored, so a stray
+// environment variable cannot change results. Tuning knobs that select between
+// equivalent algorithms (tile sizes, lane shapes) are read in every build.
+inline const char* profiling_env(const char* name) {
+#ifdef HDDM_PROFILING
+  return std::getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
 
 // ------------------------------------------------------------------ symbolic
 // One node of the nested-dissection tree produced by the reference's nd_rec

@@ -188,6 +188,7 @@ struct StepArgs {
 void launch_fany(const StepArgs& A, cudaStream_t st);
 void launch_flags(const StepArgs& A, int ncls, cudaStream_t st);
 void launch_gather(const StepArgs& A, cudaStream_t st);
+void launch_transfer(const StepArgs& A, cudaStream_t st);  // the 8-direction transfer pass alone
 void launch_accumulate(const StepArgs& A, cudaStream_t st);
 
 // per-RHS residual check of the local solve (refine's first pass,

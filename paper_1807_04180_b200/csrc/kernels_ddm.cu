@@ -193,6 +193,11 @@ __global__ void __launch_bounds__(256, HDDM_XFER_MINB) k_rhs_transfer(StepArgs A
     vview(A.B, A.vm, t)[A.pinv[node]] = cmk(0, 0);
 }
 
+void launch_transfer(const StepArgs& A, cudaStream_t st) {
+  dim3 g2((A.npatch + 255) / 256, A.nsub);
+  k_rhs_transfer<<<g2, 256, 0, st>>>(A);
+}
+
 void launch_gather(const StepArgs& A, cudaStream_t st) {
   // steps >= 2 see no f: every base value is 0. Step 2 clears all of B at memset
   // speed (right-hand sides of inactive subdomains are never read); from step 3
@@ -350,11 +355,15 @@ __device__ __forceinline__ void check_block(const CheckArgs& A, int c, int k0, i
 
 __global__ void k_finish_init(CheckArgs A, RefineArgs R, int* done);
 
-// all members of class blockIdx.y
+// all members of class blockIdx.y, 256 at a time (a thread per member and position)
 __global__ void __launch_bounds__(256, HDDM_CHECK_MINB) k_check(CheckArgs A) {
   __shared__ double sr[256], sb[256];
   const int c = blockIdx.y;
-  check_block(A, c, 0, A.vm.cptr[c + 1] - A.vm.cptr[c], sr, sb);
+  const int m = A.vm.cptr[c + 1] - A.vm.cptr[c];
+  for (int k0 = 0; k0 < m; k0 += 256) {
+    check_block(A, c, k0, min(256, m - k0), sr, sb);
+    __syncthreads();
+  }
 }
 
 // the members of tile blockIdx.y of a tile group (right after that group's solve)

@@ -153,6 +153,7 @@ def load_library(path: str = LIB_PATH):
         "hddm_time_solve": (C.c_int, [vp, C.c_int, dp]),
         "hddm_tune_fwd_shape": (C.c_int, [vp, C.c_int, C.c_int, C.c_int]),
         "hddm_solve_launches": (C.c_int, [vp]),
+        "hddm_time_kernel": (C.c_int, [vp, C.c_int, C.c_int, dp]),
         "hddm_stage_name": (C.c_char_p, [C.c_int]),
         "hddm_stream": (vp, [vp]),
         "hddm_solver_desc": (C.c_char_p, [vp]),
@@ -447,6 +448,14 @@ class DdmEngine:
     def tune_fwd_shape(self, which: int, level: int, lanes: int):
         """Tuning aid: lane shape of a steady-state forward level (hddm_tune_fwd_shape)."""
         self._check(self.lib.hddm_tune_fwd_shape(self.h, which, level, lanes))
+
+    def time_kernel(self, which: str, reps: int = 20) -> float:
+        """Device ms of one launch of a step stage kernel (transfer / check / accumulate)
+        on the last sweep's state (hddm_time_kernel)."""
+        idx = {"transfer": 0, "check": 1, "accumulate": 2}[which]
+        ms = C.c_double()
+        self._check(self.lib.hddm_time_kernel(self.h, idx, reps, C.byref(ms)))
+        return ms.value
 
     def solve_launches(self) -> int:
         return int(self.lib.hddm_solve_launches(self.h))

@@ -220,3 +220,44 @@ def test_separator_substitution_matches_inverse_path(monkeypatch):
         e.precondition(interior_random(prob4, 7), 8)
         max_rel, corrections = e.refine_stats()
     assert corrections == 0 and max_rel < 1e-11, (max_rel, corrections)
+
+
+def test_class_of_900_subdomains_matches_restatement():
+    """A 32x32 partition of a constant medium (PAPER.md:1195's scaling layout, small
+    cores): the interior class has 30 x 30 = 900 members (member tiles of <= 16; the
+    residual check takes 256 members per pass). Sweeps against the C restatement."""
+    import pyoracle
+    from paper_1807_04180_b200.engine import DdmEngine, DdmStats
+    from paper_1807_04180_b200.problems import small
+    prob = small(256, 32, 32, 6.0, 2, 4, source=("gaussian", 0.3, 0.6, 0.03))
+    f = prob.source_f()
+    o = pyoracle.OracleEngine(prob)
+    with DdmEngine(prob) as e:
+        ci = e.class_info()
+        assert max(c["members"] for c in ci) == 900 and sum(c["members"] for c in ci) == 1024
+        for K in (1, 3):
+            st, so = DdmStats(), pyoracle.Stats()
+            z = e.precondition(f, K, st)
+            zo = o.precondition(f, K, so)
+            assert rel_l2(z, zo) <= 1e-10, K
+            assert (st.solves, st.skipped) == (so.solves, so.skipped)
+    o.close()
+
+
+def test_401_window_matches_restatement():
+    """One 401 x 401 window (fronts of ~600 rows: the factorization's shared scratch is
+    sized from the largest front) against the C restatement."""
+    import pyoracle
+    from paper_1807_04180_b200.engine import DdmEngine, DdmStats
+    from paper_1807_04180_b200.problems import small
+    prob = small(352, 1, 1, 10.0, 4, 20, source=("gaussian", 0.45, 0.55, 0.02))
+    assert prob.window == (401, 401)
+    f = prob.source_f()
+    o = pyoracle.OracleEngine(prob)
+    with DdmEngine(prob) as e:
+        st = DdmStats()
+        u = e.solve_iterative(f, 1e-10, 2, st)
+        uo, so = o.solve_iterative(f, 1e-10, 2)
+        assert rel_l2(u, uo) <= 1e-10
+        assert st.steps == so.steps == 1 and st.converged
+    o.close()
