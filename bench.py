@@ -133,9 +133,10 @@ def barrier(world: int):
         dist.barrier()
 
 
-def solve_traffic():
-    """Solve-stage DRAM bytes per solve from the committed ncu step summary."""
-    path = os.path.join(ROOT, "profiles", "r01_step_summary.json")
+def solve_traffic(cfg: int):
+    """Solve-stage DRAM bytes per solve from the committed ncu step summary of this
+    config (profiles/r02_step_summary_cfg<N>.json, tools/ncu_step.py)."""
+    path = os.path.join(ROOT, "profiles", f"r02_step_summary_cfg{cfg}.json")
     try:
         with open(path) as f:
             return json.load(f)["solve_dram_bytes"]
@@ -347,10 +348,10 @@ def run_ours(args, world, rank, local):
             "munknown_iters_per_s": value * prob.n_global / 1e6,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None,
-                         "traffic": solve_traffic(),
+                         "traffic": solve_traffic(args.config),
                          "traffic_note": "DRAM bytes of the solve-stage kernels of one step, "
-                                         "profiles/r01_step_summary.json (ncu, cache flushed "
-                                         "per launch: an upper bound)",
+                                         f"profiles/r02_step_summary_cfg{args.config}.json (ncu "
+                                         "launch list, cache flushed per launch: an upper bound)",
                          "kernel": "batched supernodal solve stage (fwd+bwd, all classes)",
                          "bytes_per_launch": B["B_solve"], "ms_per_launch": solve_ms_per,
                          "peak_kind": peak_kind},
