@@ -1024,18 +1024,19 @@ static cplx vdot(const cplx* a, const cplx* b, size_t n) {
   return s;
 }
 
-/* fgmres, krylov.cpp:24-133, with A = apply_global and M = precondition(K)
- * (cli.cpp:217-222). zs (optional) receives each preconditioner output. */
-int orc_fgmres(orc_engine* e, const double* bd, double* xd, double tol,
-               int max_iters, int restart, int K, orc_fgmres_out* res,
-               double* hist, int hist_cap, double* zs, int zs_cap,
-               orc_stats* pst) {
-  const size_t n = (size_t)e->g.gnx * e->g.gny;
+/* fgmres, krylov.cpp:24-133, over caller operators A and M (ctx-bound); the
+ * 2-D engine wires A = apply_global and M = precondition(K) (cli.cpp:217-222),
+ * the 3-D extension (hddm_oracle3.c) its own pair. zs (optional) receives each
+ * preconditioner output. */
+typedef void (*orc_op_fn)(void* ctx, const cplx* in, cplx* out);
+static int fgmres_core(size_t n, orc_op_fn Aop, orc_op_fn Mop, void* ctx,
+                       const double* bd, double* xd, double tol, int max_iters,
+                       int restart, orc_fgmres_out* res, double* hist, int hist_cap,
+                       double* zs, int zs_cap) {
   const cplx* b = (const cplx*)bd;
   cplx* x = (cplx*)xd;
   const double tstart = now_ms();
   memset(res, 0, sizeof *res);
-  memset(pst, 0, sizeof *pst);
   res->relres = res->true_relres = -1;
   memset(x, 0, n * sizeof(cplx));
   const double bnorm = vnrm2(b, n);
@@ -1072,11 +1073,11 @@ int orc_fgmres(orc_engine* e, const double* bd, double* xd, double tol,
     g[0] = rnorm;
     int k = 0;
     for (int j = 0; j < m; ++j) {
-      orc_precondition(e, (const double*)V[j], (double*)Z[j], K, pst);
+      Mop(ctx, V[j], Z[j]);
       if (zs && nz < zs_cap) memcpy(zs + 2 * n * (size_t)nz, Z[j], n * sizeof(cplx));
       ++nz;
       cplx* w = V[j + 1];
-      op_apply(&e->gop, Z[j], w);
+      Aop(ctx, Z[j], w);
       cplx* Hj = H + (size_t)j * (mcap + 1);
       for (int i = 0; i <= j; ++i) {
         const cplx hij = vdot(V[i], w, n);
@@ -1132,12 +1133,12 @@ int orc_fgmres(orc_engine* e, const double* bd, double* xd, double tol,
         for (size_t t = 0; t < n; ++t) x[t] += y[l] * Z[l][t];
     }
     if (!stop) {
-      op_apply(&e->gop, x, r);
+      Aop(ctx, x, r);
       for (size_t t = 0; t < n; ++t) r[t] = b[t] - r[t];
     }
   }
   res->iters = total;
-  op_apply(&e->gop, x, r);
+  Aop(ctx, x, r);
   double s = 0;
   for (size_t t = 0; t < n; ++t) s += cnorm(b[t] - r[t]);
   res->true_relres = sqrt(s) / bnorm;
@@ -1147,3 +1148,29 @@ int orc_fgmres(orc_engine* e, const double* bd, double* xd, double tol,
   free(V); free(Z); free(H); free(g); free(sn); free(cs); free(y); free(r);
   return 0;
 }
+
+typedef struct {
+  orc_engine* e;
+  int K;
+  orc_stats* pst;
+} fgm2_ctx;
+static void fgm2_A(void* c, const cplx* in, cplx* out) {
+  op_apply(&((fgm2_ctx*)c)->e->gop, in, out);
+}
+static void fgm2_M(void* c, const cplx* in, cplx* out) {
+  fgm2_ctx* x = (fgm2_ctx*)c;
+  orc_precondition(x->e, (const double*)in, (double*)out, x->K, x->pst);
+}
+
+int orc_fgmres(orc_engine* e, const double* bd, double* xd, double tol,
+               int max_iters, int restart, int K, orc_fgmres_out* res,
+               double* hist, int hist_cap, double* zs, int zs_cap,
+               orc_stats* pst) {
+  memset(pst, 0, sizeof *pst);
+  fgm2_ctx c = {e, K, pst};
+  return fgmres_core((size_t)e->g.gnx * e->g.gny, fgm2_A, fgm2_M, &c, bd, xd, tol,
+                     max_iters, restart, res, hist, hist_cap, zs, zs_cap);
+}
+
+/* the 3-D extension (BASELINE config 5; no reference exists) */
+#include "hddm_oracle3.c"

@@ -90,6 +90,41 @@ int orc_nd_order(int nx, int ny, int* order);
  * last reset (test infrastructure) */
 void orc_refine_stats(long* ncorr, double* max_first_rel, int reset);
 
+
+/* ---- 3-D extension (BASELINE config 5; hddm_oracle3.c). PARITY UNPINNED: the
+ * reference has no 3-D code; this is the generalization PAPER.md:829 describes,
+ * written out in hddm_oracle3.c's header, and the specification the GPU engine's
+ * 3-D path is checked against. Global fields are x fastest, then y, then z. */
+typedef struct {
+  double x0, y0, z0, h;
+  int mx, my, mz, n1, n2, n3, n_overlap, n_ramp;
+  double omega, velocity; /* constant medium */
+  double c_sigma, sigma0;
+} orc3_problem;
+
+typedef struct orc3_engine orc3_engine;
+int orc3_create(const orc3_problem* p, orc3_engine** out);
+void orc3_destroy(orc3_engine* e);
+long orc3_n_global(const orc3_engine* e);
+double orc3_sigma0(const orc3_engine* e);
+int orc3_num_classes(const orc3_engine* e);
+int orc3_class_of(const orc3_engine* e, int t);
+int orc3_window_dims(const orc3_engine* e, int* nn);
+int orc3_class_info(const orc3_engine* e, int c, int* members, long* nnz, double* probe);
+int orc3_class_solve(const orc3_engine* e, int c, const double* b, double* x, double* relres);
+int orc3_class_matvec(const orc3_engine* e, int c, const double* x, double* y);
+int orc3_apply_global(const orc3_engine* e, const double* u, double* out);
+int orc3_solve_iterative(orc3_engine* e, const double* f, double tol, int max_steps,
+                         int check_every, double* out, orc_stats* st, int* hist_step,
+                         double* hist_rel, int hist_cap, int* hist_len);
+int orc3_precondition(orc3_engine* e, const double* r, double* z, int k, orc_stats* st);
+int orc3_fgmres(orc3_engine* e, const double* b, double* x, double tol, int max_iters,
+                int restart, int K, orc_fgmres_out* res, double* hist, int hist_cap,
+                double* zs, int zs_cap, orc_stats* pst);
+int orc3_tap_subdomain(const orc3_engine* e, int t, double* rhs, double* u, int* active);
+int orc3_nd_order(int nx, int ny, int nz, int* order);
+int orc3_direction(int d, int* o);
+
 #ifdef __cplusplus
 }
 #endif

@@ -320,3 +320,127 @@ def ref_direct_solve(prob, f) -> np.ndarray:
         raise RuntimeError(lib.ref_last_error().decode())
     del eng
     return out
+
+
+# ------------------------------------------------------------------ 3-D
+class _Problem3(C.Structure):
+    _fields_ = [
+        ("x0", C.c_double), ("y0", C.c_double), ("z0", C.c_double), ("h", C.c_double),
+        ("mx", C.c_int), ("my", C.c_int), ("mz", C.c_int),
+        ("n1", C.c_int), ("n2", C.c_int), ("n3", C.c_int),
+        ("n_overlap", C.c_int), ("n_ramp", C.c_int),
+        ("omega", C.c_double), ("velocity", C.c_double),
+        ("c_sigma", C.c_double), ("sigma0", C.c_double),
+    ]
+
+
+def _lib3():
+    lib = _lib("orc")
+    if getattr(lib, "_have3", False):
+        return lib
+    P = C.POINTER
+    d = C.c_double
+    dp = P(C.c_double)
+    vp = C.c_void_p
+    ip = P(C.c_int)
+    sig = {
+        "create": (C.c_int, [P(_Problem3), P(vp)]),
+        "destroy": (None, [vp]),
+        "n_global": (C.c_long, [vp]),
+        "sigma0": (d, [vp]),
+        "num_classes": (C.c_int, [vp]),
+        "class_of": (C.c_int, [vp, C.c_int]),
+        "window_dims": (C.c_int, [vp, ip]),
+        "class_info": (C.c_int, [vp, C.c_int, ip, P(C.c_long), dp]),
+        "class_solve": (C.c_int, [vp, C.c_int, dp, dp, dp]),
+        "class_matvec": (C.c_int, [vp, C.c_int, dp, dp]),
+        "apply_global": (C.c_int, [vp, dp, dp]),
+        "solve_iterative": (C.c_int, [vp, dp, d, C.c_int, C.c_int, dp, P(_Stats), ip, dp,
+                                      C.c_int, ip]),
+        "precondition": (C.c_int, [vp, dp, dp, C.c_int, P(_Stats)]),
+        "fgmres": (C.c_int, [vp, dp, dp, d, C.c_int, C.c_int, C.c_int, P(_FgOut), dp,
+                             C.c_int, dp, C.c_int, P(_Stats)]),
+        "tap_subdomain": (C.c_int, [vp, C.c_int, dp, dp, ip]),
+        "nd_order": (C.c_int, [C.c_int, C.c_int, C.c_int, ip]),
+        "direction": (C.c_int, [C.c_int, ip]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, f"orc3_{name}")
+        fn.restype = res
+        fn.argtypes = args
+    lib._have3 = True
+    return lib
+
+
+class Oracle3Engine(_Engine):
+    """The 3-D extension of the restatement (oracle/hddm_oracle3.c). Parity
+    unpinned: the reference has no 3-D code."""
+    prefix = "orc3"
+
+    def __init__(self, prob):  # noqa: D401 -- same surface as _Engine
+        self.prob = prob
+        self.lib = _lib3()
+        fn = lambda n: getattr(self.lib, f"orc3_{n}") if n != "last_error" else self.lib.orc_last_error
+        self._fn = fn
+        P = _Problem3()
+        P.x0, P.y0, P.z0, P.h = prob.x0, prob.y0, prob.z0, prob.h
+        P.mx, P.my, P.mz = prob.mx, prob.my, prob.mz
+        P.n1, P.n2, P.n3 = prob.n1, prob.n2, prob.n3
+        P.n_overlap, P.n_ramp = prob.n_overlap, prob.n_ramp
+        P.omega, P.velocity = prob.omega, prob.velocity
+        P.c_sigma, P.sigma0 = prob.c_sigma, prob.sigma0
+        self._P = P
+        h = C.c_void_p()
+        rc = fn("create")(C.byref(P), C.byref(h))
+        if rc != 0:
+            raise RuntimeError(f"orc3_create failed ({rc}): {fn('last_error')().decode()}")
+        self.h = h
+        self.n = int(fn("n_global")(h))
+        nn = np.zeros(3, np.int32)
+        fn("window_dims")(h, nn.ctypes.data_as(C.POINTER(C.c_int)))
+        self.window = tuple(int(v) for v in nn)
+
+    def class_info(self):
+        out = []
+        for c in range(self._fn("num_classes")(self.h)):
+            m, nnz, pr = C.c_int(), C.c_long(), C.c_double()
+            self._check(self._fn("class_info")(self.h, c, C.byref(m), C.byref(nnz), C.byref(pr)))
+            out.append(dict(members=m.value, factor_nnz=nnz.value, probe_relres=pr.value,
+                            backend="ldlt"))
+        return out
+
+    def class_of(self, t: int) -> int:
+        return int(self._fn("class_of")(self.h, t))
+
+    def class_solve(self, c: int, b):
+        b = _cvec(b)
+        x = np.empty_like(b)
+        rel = C.c_double()
+        self._check(self._fn("class_solve")(self.h, c, _dp(b), _dp(x), C.byref(rel)))
+        return x, rel.value
+
+    def class_matvec(self, c: int, x):
+        x = _cvec(x)
+        y = np.empty_like(x)
+        self._check(self._fn("class_matvec")(self.h, c, _dp(x), _dp(y)))
+        return y
+
+    def tap_subdomain(self, t: int):
+        nw = int(np.prod(self.window))
+        rhs = np.zeros(nw, np.complex128)
+        u = np.zeros(nw, np.complex128)
+        act = C.c_int()
+        self._check(self._fn("tap_subdomain")(self.h, t, _dp(rhs), _dp(u), C.byref(act)))
+        return rhs, u, bool(act.value)
+
+
+def nd_order3(nx: int, ny: int, nz: int) -> np.ndarray:
+    out = np.zeros(nx * ny * nz, np.int32)
+    _lib3().orc3_nd_order(nx, ny, nz, out.ctypes.data_as(C.POINTER(C.c_int)))
+    return out
+
+
+def direction3(d: int):
+    o = np.zeros(3, np.int32)
+    _lib3().orc3_direction(d, o.ctypes.data_as(C.POINTER(C.c_int)))
+    return tuple(int(v) for v in o)

@@ -18,6 +18,8 @@ cfg    geometry / medium / source                                   run
 3      1024^2, 8x8, lens c=1-0.4exp(-r^2/0.05), w=120pi, s=.005@(.25,.25)  FGMRES(30)+DDM(K=16)
 4      2048^2, 16x16, ov 8, PML 24, 20 random layers (mt19937_64 seed 0),
        w = 2pi c_min 2048/8, s=0.003 @ (0.5, 0.1)                   FGMRES(30)+DDM(K=32)
+5      3-D 64^3, 2x2x2, ov 4, PML 8, c=1, w=16pi, 3-D Gaussian
+       s=0.02 at the cube centre (``Problem3``; no reference)       FGMRES(30)+DDM(K=6)
 =====  ===========================================================  =========
 
 ``h = 1/mx`` for cfg 1: "256x256 interior, h=1/257" cannot be split four ways;
@@ -221,7 +223,9 @@ def config(n: int) -> Problem:
                        medium_kind=MEDIUM_LAYERED, layers=layers,
                        source=("gaussian", 0.5, 0.1, 0.003), mode="fgmres",
                        tol=1e-6, K=32, restart=30, max_iters=200)
-    raise ValueError(f"config {n} not available (3D config 5 is SURVEY 8(f) 'next')")
+    if n == 5:
+        return config5()
+    raise ValueError(f"config {n} not available (configs 1-5)")
 
 
 def small(mx: int = 40, n1: int = 2, n2: int = 2, freq: float = 4.0, n_ov: int = 4,
@@ -229,3 +233,111 @@ def small(mx: int = 40, n1: int = 2, n2: int = 2, freq: float = 4.0, n_ov: int =
     """The reference tests' ``make_cfg`` (proj/tests/test_ddm.cpp:15-30)."""
     return Problem(f"small_{mx}_{n1}x{n2}", mx=mx, n1=n1, n2=n2, n_overlap=n_ov,
                    n_ramp=n_ramp, omega=2 * math.pi * freq, source=source, **kw)
+
+
+@dataclass
+class Problem3:
+    """A 3-D problem (BASELINE config 5): the 2-D ``Problem`` with a third axis
+    and a constant medium. The reference has no 3-D code; the
+    formulas are the generalization written out in oracle/hddm_oracle3.c."""
+    name: str
+    mx: int
+    n1: int
+    n2: int
+    n3: int
+    n_overlap: int
+    n_ramp: int
+    omega: float
+    my: int = 0
+    mz: int = 0
+    h: float = 0.0
+    x0: float = 0.0
+    y0: float = 0.0
+    z0: float = 0.0
+    velocity: float = 1.0
+    c_sigma: float = 25.0
+    sigma0: float = 0.0
+    source: Tuple = ("gaussian", 0.5, 0.5, 0.5, 0.02)  # exp(-r^2 / (2 sigma^2))
+    mode: str = "fgmres"
+    steps: int = 10
+    tol: float = 1e-6
+    K: int = 0                # 0 -> n1 + n2 + n3 (PAPER.md:829)
+    restart: int = 30
+    max_iters: int = 200
+
+    def __post_init__(self):
+        if self.my == 0:
+            self.my = self.mx
+        if self.mz == 0:
+            self.mz = self.mx
+        if self.h == 0.0:
+            self.h = 1.0 / self.mx
+
+    @property
+    def n_ext(self) -> int:
+        return self.n_overlap + self.n_ramp
+
+    @property
+    def gdims(self) -> Tuple[int, int, int]:
+        e = 2 * self.n_ext + 1
+        return (self.mx + e, self.my + e, self.mz + e)
+
+    @property
+    def n_global(self) -> int:
+        a, b, c = self.gdims
+        return a * b * c
+
+    @property
+    def window(self) -> Tuple[int, int, int]:
+        e = 2 * self.n_ext + 1
+        return (self.mx // self.n1 + e, self.my // self.n2 + e, self.mz // self.n3 + e)
+
+    @property
+    def nsub(self) -> int:
+        return self.n1 * self.n2 * self.n3
+
+    @property
+    def k_steps(self) -> int:
+        return self.K if self.K > 0 else self.n1 + self.n2 + self.n3
+
+    def source_f(self) -> np.ndarray:
+        """Global-window source, complex128, x fastest then y then z."""
+        gx, gy, gz = self.gdims
+        e = self.n_ext * self.h
+        xs = self.x0 - e + np.arange(gx) * self.h
+        ys = self.y0 - e + np.arange(gy) * self.h
+        zs = self.z0 - e + np.arange(gz) * self.h
+        kind = self.source[0]
+        if kind == "gaussian":
+            _, xc, yc, zc, sig = self.source
+            r2 = ((zs - zc) ** 2)[:, None, None] + ((ys - yc) ** 2)[None, :, None] + \
+                ((xs - xc) ** 2)[None, None, :]
+            return np.exp(-r2 / (2.0 * sig * sig)).astype(np.complex128).ravel()
+        if kind == "point":
+            _, x, y, z = self.source
+            f = np.zeros((gz, gy, gx), np.complex128)
+            idx = [int(math.ceil((v - (o - e)) / self.h - 0.5)) for v, o in
+                   ((x, self.x0), (y, self.y0), (z, self.z0))]
+            if 0 <= idx[0] < gx and 0 <= idx[1] < gy and 0 <= idx[2] < gz:
+                f[idx[2], idx[1], idx[0]] = 1.0 / (self.h ** 3)
+            return f.ravel()
+        raise ValueError(f"unknown source kind {kind!r}")
+
+    def with_(self, **kw) -> "Problem3":
+        return replace(self, **kw)
+
+
+def config5() -> Problem3:
+    """BASELINE config 5: 64^3, 2x2x2, overlap 4, PML 8, c=1, w=16pi, 3-D
+    Gaussian sigma=0.02 at the centre, FGMRES(30)+DDM(K=6) to 1e-6
+    (SURVEY.md 8(d))."""
+    return Problem3("cfg5_64cube_2x2x2_fgmres", mx=64, n1=2, n2=2, n3=2, n_overlap=4,
+                    n_ramp=8, omega=16 * math.pi, source=("gaussian", 0.5, 0.5, 0.5, 0.02),
+                    mode="fgmres", tol=1e-6, K=6, restart=30, max_iters=200)
+
+
+def small3(m: int = 16, n: int = 2, freq: float = 3.0, n_ov: int = 2, n_ramp: int = 3,
+           source=("gaussian", 0.45, 0.55, 0.5, 0.08), **kw) -> Problem3:
+    """A small 3-D case the C restatement factors in well under a second."""
+    return Problem3(f"small3_{m}_{n}", mx=m, n1=n, n2=n, n3=n, n_overlap=n_ov,
+                    n_ramp=n_ramp, omega=2 * math.pi * freq, source=source, **kw)
