@@ -86,3 +86,47 @@ def step_bytes(p: Problem, nnz_per_class, members_per_class, standalone: bool = 
     out["B_solve"] = b_fac + b_vec
     out["B_step"] = b_fac + b_vec + b_xfer + b_acc + b_res
     return out
+
+
+def step_bytes3(p, nnz_per_class) -> Dict[str, float]:
+    """The same count for a 3-D problem (Problem3, config 5): 26 transfer
+    directions (hddm_oracle3.c transfer_patch3), box blend regions."""
+    ext, nov = p.n_ext, p.n_overlap
+    nd = (p.n1, p.n2, p.n3)
+    mc = (p.mx // p.n1, p.my // p.n2, p.mz // p.n3)
+    nn = p.window
+    nw = nn[0] * nn[1] * nn[2]
+    nsub = p.nsub
+    b_fac = sum(16.0 * (2.0 * (nnz - nw) + nw) for nnz in nnz_per_class)
+    b_vec = 2.0 * 16.0 * nw * nsub
+    dirs = [(a, b, c) for c in (-1, 0, 1) for b in (-1, 0, 1) for a in (-1, 0, 1) if (a, b, c) != (0, 0, 0)]
+    b_xfer = b_acc = 0.0
+    for t in range(nsub):
+        ix = (t % nd[0], (t // nd[0]) % nd[1], t // (nd[0] * nd[1]))
+        c0 = [ext + ix[a] * mc[a] for a in range(3)]
+        c1 = [c0[a] + mc[a] for a in range(3)]
+        w0 = [c0[a] - ext for a in range(3)]
+        for o in dirs:
+            if not all(0 <= ix[a] + o[a] < nd[a] for a in range(3)):
+                continue
+            vol = wvol = 1
+            for a in range(3):
+                lo, hi = w0[a] + 1, w0[a] + nn[a] - 2
+                if o[a] > 0:
+                    lo, hi = max(lo, c1[a] - 1 - nov), min(hi, c1[a] - 1)
+                elif o[a] < 0:
+                    lo, hi = max(lo, c0[a] + 1), min(hi, c0[a] + 1 + nov)
+                vol *= max(0, hi - lo + 1)
+                wvol *= max(0, hi - lo + 3)
+            if vol:
+                b_xfer += 16.0 * (vol + wvol)
+        reg = 1
+        for a in range(3):
+            x0 = c0[a] - nov if ix[a] > 0 else w0[a]
+            x1 = c1[a] + nov if ix[a] < nd[a] - 1 else w0[a] + nn[a] - 1
+            reg *= x1 - x0 + 1
+        b_acc += 48.0 * reg
+    out = dict(B_fac=b_fac, B_vec=b_vec, B_xfer=b_xfer, B_acc=b_acc, B_res=0.0)
+    out["B_solve"] = b_fac + b_vec
+    out["B_step"] = b_fac + b_vec + b_xfer + b_acc
+    return out
