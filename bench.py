@@ -208,10 +208,117 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def dense_residual3(prob, seed: int = 1234) -> np.ndarray:
+    """dense_residual for a 3-D problem: zero on the global boundary shell."""
+    rng = np.random.default_rng(seed)
+    gx, gy, gz = prob.gdims
+    r = rng.standard_normal((gz, gy, gx)) + 1j * rng.standard_normal((gz, gy, gx))
+    r[0], r[-1] = 0, 0
+    r[:, 0], r[:, -1] = 0, 0
+    r[:, :, 0], r[:, :, -1] = 0, 0
+    r = r.ravel()
+    return r / np.linalg.norm(r)
+
+
+def run_ours3(args, world, rank, local):
+    """Config 5 (3-D, include/hddm3.h): the same measurements as run_ours."""
+    import torch
+    from paper_1807_04180_b200.engine import DdmStats, FgmresOptions
+    from paper_1807_04180_b200.engine3 import DdmEngine3
+    from paper_1807_04180_b200.roofline import step_bytes3
+
+    prob = config(5)
+    torch.cuda.set_device(local)
+    eng = DdmEngine3(prob, device=local)
+    ci = eng.class_info()
+    r = torch.from_numpy(dense_residual3(prob)).to(f"cuda:{local}")
+    z = torch.empty_like(r)
+    stream = torch.cuda.ExternalStream(eng.stream_handle(), device=f"cuda:{local}")
+    eng.precondition(r, max(args.warmup, 1), DdmStats(), out=z)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    eng.set_timing(True)
+    barrier(world)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    st = DdmStats()
+    e0.record(stream)
+    eng.precondition(r, args.steps, st, out=z)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = e0.elapsed_time(e1)
+    clocks = sampler.stop()
+    launches = eng.launch_count()
+    max_local_rel, corrections = eng.refine_stats()
+    solve_ms_per = eng.time_solve(max(5, args.steps))
+    ms_max = allreduce_max(ms, world)
+    value = world * args.steps / (ms_max / 1e3)
+    peak, peak_kind = measured_peaks()
+    nnz = [c["factor_nnz"] for c in ci]
+    B = step_bytes3(prob, nnz)
+    achieved = B["B_solve"] / (solve_ms_per / 1e3) / 1e9
+    step_achieved = B["B_step"] / (ms / args.steps / 1e3) / 1e9
+    e2e = None
+    if not args.skip_e2e:
+        f_host = prob.source_f()
+        nbytes = 16 * prob.n_global
+        eng.fgmres(f_host, FgmresOptions(prob.tol, 1, prob.restart), prob.k_steps)
+        K = prob.k_steps
+        t0 = time.perf_counter()
+        x, res = eng.fgmres(f_host, FgmresOptions(prob.tol, prob.max_iters, prob.restart), K)
+        wall = time.perf_counter() - t0
+        total_steps = res.iters * K
+        e2e = {"value": world * total_steps / wall, "unit": UNIT,
+               "h2d_bytes_per_step": nbytes / max(total_steps, 1),
+               "d2h_bytes_per_step": nbytes / max(total_steps, 1),
+               "what": f"FGMRES({prob.restart})+DDM(K={K}) to {prob.tol} from host b to host x",
+               "gmres_iters": res.iters, "ddm_steps": total_steps,
+               "true_relres": res.true_relres, "wall_s": wall}
+    fp = eng.footprint()
+    if rank == 0:
+        gx, gy, gz = prob.gdims
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": prob.name, "grid": f"{prob.mx}x{prob.my}x{prob.mz}",
+                       "subdomains": f"{prob.n1}x{prob.n2}x{prob.n3}", "n_global": prob.n_global,
+                       "classes": len(ci), "parallelism": f"replicas x{world}",
+                       "l2": f"factors {16 * sum(nnz) / 1e9:.1f} GB vs 126 MB L2: no flush",
+                       "step": "one DDM sweep of precondition(r, K=steps), dense r"},
+            "munknown_iters_per_s": value * prob.n_global / 1e6,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "batched dense supernodal solve stage (fwd+bwd, all classes)",
+                         "bytes_per_launch": B["B_solve"], "ms_per_launch": solve_ms_per,
+                         "peak_kind": peak_kind},
+            "step_roofline": {"achieved_gbs": step_achieved, "bytes_per_step": B["B_step"],
+                              "frac": step_achieved / peak},
+            "factor": {"ms": eng.factor_ms(), "classes": len(ci),
+                       "stored_values_per_class": fp["stored_values_per_class"],
+                       "ref_nnz_per_class": fp["ref_nnz_per_class"],
+                       "factor_bytes": 16 * fp["stored_values_per_class"] * len(ci),
+                       "device_bytes_in_use": fp["device_bytes_in_use"], "hbm_bytes": 180e9},
+            "solve_launches_per_step": eng.solve_launches(),
+            "refine": {"max_first_pass_relres": max_local_rel, "solves_corrected": corrections},
+            "cpu_baseline": None,
+            "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
+            "solves": st.solves, "skipped": st.skipped,
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+
+
 def run_ours(args, world, rank, local):
     import torch
     from paper_1807_04180_b200.engine import DdmEngine, DdmStats, FgmresOptions
 
+    if args.config == 5:
+        return run_ours3(args, world, rank, local)
     prob = config(args.config)
     torch.cuda.set_device(local)
     eng = DdmEngine(prob, device=local)

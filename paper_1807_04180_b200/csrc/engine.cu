@@ -71,8 +71,8 @@ struct hddm_engine {
   long long ng = 0;
   double factor_ms = 0;
   std::vector<double> probe;
-  size_t dev_bytes = 0;
-  std::vector<void*> allocs;
+  size_t dev_bytes = 0;  // bytes currently allocated
+  std::vector<std::pair<void*, size_t>> allocs;
   int last_step = 0;
   double last_max_rel = 0;
   int last_refine_count = 0;
@@ -199,13 +199,16 @@ struct hddm_engine {
   T* dalloc(size_t n) {
     void* p = nullptr;
     CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
-    allocs.push_back(p);
+    allocs.push_back({p, std::max<size_t>(n, 1) * sizeof(T)});
     dev_bytes += std::max<size_t>(n, 1) * sizeof(T);
     return static_cast<T*>(p);
   }
   void dfree(void* p) {
-    auto it = std::find(allocs.begin(), allocs.end(), p);
-    if (it != allocs.end()) allocs.erase(it);
+    auto it = std::find_if(allocs.begin(), allocs.end(), [p](const auto& a) { return a.first == p; });
+    if (it != allocs.end()) {
+      dev_bytes -= it->second;
+      allocs.erase(it);
+    }
     cudaFree(p);
   }
   template <class T>
@@ -218,7 +221,7 @@ struct hddm_engine {
 
   ~hddm_engine() {
     if (dev >= 0) cudaSetDevice(dev);
-    for (void* p : allocs) cudaFree(p);
+    for (auto& a : allocs) cudaFree(a.first);
     for (auto& e : ev_pool) cudaEventDestroy(e);
     if (h_scal) cudaFreeHost(h_scal);
     if (h_ks) cudaFreeHost(h_ks);

@@ -50,7 +50,6 @@ inline cplx cmk3(double r, double i) { return make_double2(r, i); }
 
 constexpr int kChunks = 32;    // residual-check partials per RHS
 constexpr int kDiagRows = 32;  // rows per forward inverse / panel task
-constexpr int kColTask = 8;    // columns per backward task (warp per column)
 
 }  // namespace
 
@@ -64,8 +63,8 @@ struct hddm3_engine {
   long long ng = 0;
   double factor_ms = 0;
   std::vector<double> probe;
-  size_t dev_bytes = 0;
-  std::vector<void*> allocs;
+  size_t dev_bytes = 0;  // bytes currently allocated
+  std::vector<std::pair<void*, size_t>> allocs;
   long long launches = 0;
   int last_step = 0;
   double last_max_rel = 0;
@@ -77,9 +76,10 @@ struct hddm3_engine {
   int *d_perm = nullptr, *d_pinv = nullptr;
   int *d_cls_ptr = nullptr, *d_cls_mem = nullptr;
   cplx* d_vals = nullptr;
+  cplx* d_valsT = nullptr;  // backward (row-major) copy of the blocks
   struct Lvl {
     Task3* d = nullptr;
-    int n = 0;
+    int n = 0, nbig = 0;
   };
   std::vector<Lvl> f_asm, f_diag, f_pan, b_gat, b_pan, b_diag;
   // per subdomain
@@ -117,14 +117,18 @@ struct hddm3_engine {
   template <class T>
   T* dalloc(size_t n) {
     void* p = nullptr;
-    CK3(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
-    allocs.push_back(p);
-    dev_bytes += std::max<size_t>(n, 1) * sizeof(T);
+    const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+    CK3(cudaMalloc(&p, bytes));
+    allocs.push_back({p, bytes});
+    dev_bytes += bytes;
     return static_cast<T*>(p);
   }
   void dfree(void* p) {
-    auto it = std::find(allocs.begin(), allocs.end(), p);
-    if (it != allocs.end()) allocs.erase(it);
+    auto it = std::find_if(allocs.begin(), allocs.end(), [p](const auto& a) { return a.first == p; });
+    if (it != allocs.end()) {
+      dev_bytes -= it->second;
+      allocs.erase(it);
+    }
     cudaFree(p);
   }
   template <class T>
@@ -136,7 +140,7 @@ struct hddm3_engine {
   }
   ~hddm3_engine() {
     if (dev >= 0) cudaSetDevice(dev);
-    for (void* p : allocs) cudaFree(p);
+    for (auto& a : allocs) cudaFree(a.first);
     if (h_scal) cudaFreeHost(h_scal);
     if (h_ks) cudaFreeHost(h_ks);
     if (kry_exec) cudaGraphExecDestroy(kry_exec);
@@ -348,43 +352,77 @@ void hddm3_engine::create(const hddm3_problem& p) {
 }
 
 // Task lists: forward levels by height (leaves first), backward levels by depth.
+// Forward inverse / panel rows of supernodes with more than kSmallCols columns are
+// CTA tasks (8 warps split the columns); the others warp tasks, 8 per CTA.
+constexpr int kSmallCols = 64;
+constexpr int kColsPerTask = 32;  // backward: lane = column
+
 void hddm3_engine::build_plan() {
   const int nsn = int(Y.sn.size());
-  auto up = [&](const std::vector<Task3>& v) {
+  auto task = [&](int s, int a, int b) {
+    const Sn3& x = Y.sn[s];
+    Task3 t = {};
+    t.s = s;
+    t.a = a;
+    t.b = b;
+    t.c0 = x.c0;
+    t.n = x.n;
+    t.r = int(x.rows.size());
+    t.linv = Y.linv_off[s];
+    t.pan = Y.pan_off[s];
+    t.upd = Y.upd_off[s];
+    t.cmap = Y.cmap_off[s];
+    t.rows = Y.rows_off[s];
+    return t;
+  };
+  auto up = [&](const std::vector<Task3>& v, int nbig = 0) {
     Lvl L;
     L.n = int(v.size());
+    L.nbig = nbig;
     if (L.n) L.d = upload(v);
     return L;
   };
+  // big tasks first, then the warp tasks padded to a multiple of 8
+  auto split = [&](std::vector<Task3>& big, std::vector<Task3>& small) {
+    const int nbig = int(big.size());
+    while (small.size() % 8) small.push_back(Task3{});
+    big.insert(big.end(), small.begin(), small.end());
+    return nbig;
+  };
   for (int h = 0; h <= Y.max_height; ++h) {
-    std::vector<Task3> a, d, p;
+    std::vector<Task3> a, db, ds, pb, ps;
     for (int s = 0; s < nsn; ++s) {
       const Sn3& x = Y.sn[s];
       if (x.height != h) continue;
       const int r = int(x.rows.size());
-      for (int i = 0; i < x.n; i += 256) a.push_back({s, i, std::min(x.n, i + 256), 0});
-      for (int i = 0; i < x.n; i += kDiagRows) d.push_back({s, i, std::min(x.n, i + kDiagRows), 0});
-      for (int k = 0; k < r; k += kDiagRows) p.push_back({s, k, std::min(r, k + kDiagRows), 0});
+      const bool big = x.n > kSmallCols;
+      for (int i = 0; i < x.n; i += 256) a.push_back(task(s, i, std::min(x.n, i + 256)));
+      for (int i = 0; i < x.n; i += kDiagRows) (big ? db : ds).push_back(task(s, i, std::min(x.n, i + kDiagRows)));
+      for (int k = 0; k < r; k += kDiagRows) (big ? pb : ps).push_back(task(s, k, std::min(r, k + kDiagRows)));
     }
     f_asm.push_back(up(a));
-    f_diag.push_back(up(d));
-    f_pan.push_back(up(p));
+    const int nbd = split(db, ds);
+    f_diag.push_back(up(db, nbd));
+    const int nbp = split(pb, ps);
+    f_pan.push_back(up(pb, nbp));
   }
   for (int dd = 0; dd <= Y.max_depth; ++dd) {
-    std::vector<Task3> g, p, d;
+    std::vector<Task3> g, pb, ps, db, ds;
     for (int s = 0; s < nsn; ++s) {
       const Sn3& x = Y.sn[s];
       if (x.depth != dd) continue;
       const int r = int(x.rows.size());
-      for (int k = 0; k < r; k += 256) g.push_back({s, k, std::min(r, k + 256), 0});
-      for (int j = 0; j < x.n; j += kColTask) {
-        p.push_back({s, j, std::min(x.n, j + kColTask), 0});
-        d.push_back({s, j, std::min(x.n, j + kColTask), 0});
+      for (int k = 0; k < r; k += 256) g.push_back(task(s, k, std::min(r, k + 256)));
+      for (int j = 0; j < x.n; j += kColsPerTask) {
+        (r > kSmallCols ? pb : ps).push_back(task(s, j, std::min(x.n, j + kColsPerTask)));
+        (x.n > kSmallCols ? db : ds).push_back(task(s, j, std::min(x.n, j + kColsPerTask)));
       }
     }
     b_gat.push_back(up(g));
-    b_pan.push_back(up(p));
-    b_diag.push_back(up(d));
+    const int nbp = split(pb, ps);
+    b_pan.push_back(up(pb, nbp));
+    const int nbd = split(db, ds);
+    b_diag.push_back(up(db, nbd));
   }
 }
 
@@ -439,7 +477,9 @@ void hddm3_engine::factorize() {
   int* d_aj = upload(Y.aent_j);
   int* d_ext = upload(Y.ext);
   d_vals = dalloc<cplx>(size_t(ncls) * Y.nvals);
+  d_valsT = dalloc<cplx>(size_t(ncls) * Y.nvals);
   CK3(cudaMemsetAsync(d_vals, 0, sizeof(cplx) * size_t(ncls) * Y.nvals, st));
+  CK3(cudaMemsetAsync(d_valsT, 0, sizeof(cplx) * size_t(ncls) * Y.nvals, st));
   // levels by height
   std::vector<std::vector<int>> lv(Y.max_height + 1);
   for (int s = 0; s < nsn; ++s) lv[Y.sn[s].height].push_back(s);
@@ -463,6 +503,7 @@ void hddm3_engine::factorize() {
   F.naent = naent;
   F.ext = d_ext;
   F.vals = d_vals;
+  F.valsT = d_valsT;
   F.nvals = Y.nvals;
   for (int c0 = 0; c0 < ncls; c0 += nb) {
     const int nbc = std::min(nb, ncls - c0);
@@ -514,6 +555,7 @@ Solve3Args hddm3_engine::solve_args(const cplx* B, cplx* X, const int* flag, int
   Solve3Args A;
   A.sn = d_sn;
   A.vals = d_vals;
+  A.valsT = d_valsT;
   A.nvals = Y.nvals;
   A.rows_all = d_rows;
   A.cmap0 = d_cmap0;
@@ -536,13 +578,13 @@ void hddm3_engine::enqueue_solve(const Solve3Args& A, cudaStream_t s) {
   s3_ring(A, ncls, ngroups, s);
   for (size_t h = 0; h < f_asm.size(); ++h) {
     s3_fasm(A, f_asm[h].d, f_asm[h].n, ncls, ngroups, s);
-    s3_fdiag(A, f_diag[h].d, f_diag[h].n, ncls, ngroups, s);
-    s3_fpanel(A, f_pan[h].d, f_pan[h].n, ncls, ngroups, s);
+    s3_fdiag(A, f_diag[h].d, f_diag[h].n, f_diag[h].nbig, ncls, ngroups, s);
+    s3_fpanel(A, f_pan[h].d, f_pan[h].n, f_pan[h].nbig, ncls, ngroups, s);
   }
   for (size_t d = 0; d < b_gat.size(); ++d) {
     s3_bgather(A, b_gat[d].d, b_gat[d].n, ncls, ngroups, s);
-    s3_bpanel(A, b_pan[d].d, b_pan[d].n, ncls, ngroups, s);
-    s3_bdiag(A, b_diag[d].d, b_diag[d].n, ncls, ngroups, s);
+    s3_bpanel(A, b_pan[d].d, b_pan[d].n, b_pan[d].nbig, ncls, ngroups, s);
+    s3_bdiag(A, b_diag[d].d, b_diag[d].n, b_diag[d].nbig, ncls, ngroups, s);
   }
 }
 

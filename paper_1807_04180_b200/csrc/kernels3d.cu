@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(256) k3f_extract(Fac3Args F, const int* lv) {
   const cplx* fr = F.fronts + blockIdx.z * F.fw + S.front_off;
   const long long ld = 2LL * S.n + S.r;
   cplx* v = F.vals + (long long)c * F.nvals;
+  cplx* vt = F.valsT + (long long)c * F.nvals;
   const long long nd = (long long)S.n * S.n, tot = nd + (long long)S.r * S.n;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot;
        e += (long long)gridDim.x * blockDim.x) {
@@ -245,14 +246,19 @@ __global__ void __launch_bounds__(256) k3f_extract(Fac3Args F, const int* lv) {
       const int i = int(e % S.n), j = int(e / S.n);
       if (i == j) {
         v[S.c0 + j] = fr[(long long)j * ld + j];
+        vt[S.c0 + j] = v[S.c0 + j];
       } else if (i > j) {
         const cplx di = fr[(long long)i * ld + i];
-        v[S.linv_off + colstart(j, S.n) + (i - j - 1)] = cmul(fr[(long long)i * ld + S.n + S.r + j], di);
+        const cplx x = cmul(fr[(long long)i * ld + S.n + S.r + j], di);
+        v[S.linv_off + colstart(j, S.n) + (i - j - 1)] = x;
+        vt[S.linv_off + (long long)i * (i - 1) / 2 + j] = x;
       }
     } else {
       const long long q = e - nd;
       const int k = int(q % S.r), j = int(q / S.r);
-      v[S.pan_off + (long long)j * S.r + k] = fr[(long long)j * ld + S.n + k];
+      const cplx x = fr[(long long)j * ld + S.n + k];
+      v[S.pan_off + (long long)j * S.r + k] = x;
+      vt[S.pan_off + (long long)k * S.n + j] = x;
     }
   }
 }
@@ -326,12 +332,11 @@ __global__ void __launch_bounds__(256) k3s_fasm(Solve3Args A, const Task3* tk) {
   const Mem m = members(A);
   if (!m.cnt) return;
   const Task3 T = tk[blockIdx.x];
-  const DSn3 S = A.sn[T.s];
   const int i = T.a + threadIdx.x;
   if (i >= T.b) return;
-  const int m0 = A.cmap0[S.cmap_off + i], m1 = A.cmap1[S.cmap_off + i];
+  const int m0 = A.cmap0[T.cmap + i], m1 = A.cmap1[T.cmap + i];
   for (int k = 0; k < m.cnt; ++k) {
-    const long long o = (long long)m.t[k] * A.nw + S.c0 + i;
+    const long long o = (long long)m.t[k] * A.nw + T.c0 + i;
     const cplx* u = A.U + (long long)m.t[k] * A.nupd;
     cplx y = A.B[o];
     if (m0 >= 0) y = cadd(y, u[m0]);
@@ -340,105 +345,115 @@ __global__ void __launch_bounds__(256) k3s_fasm(Solve3Args A, const Task3* tk) {
   }
 }
 
-// forward inverse rows: x_i = y_i + sum_{j<i} Linv_ij y_j. CTA per 32-row chunk:
-// lane = row, the 8 warps take interleaved 4-column groups, partials combined in
-// warp order.
-__global__ void __launch_bounds__(256) k3s_fdiag(Solve3Args A, const Task3* tk) {
-  __shared__ cplx part[8][kMG][32];
-  const Mem m = members(A);
-  if (!m.cnt) return;
-  const Task3 T = tk[blockIdx.x];
-  const DSn3 S = A.sn[T.s];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int i = T.a + lane;
-  const bool row = i < T.b;
-  const cplx* L = A.vals + (long long)blockIdx.y * A.nvals + S.linv_off;
-  const cplx* y[kMG];
-#pragma unroll
-  for (int k = 0; k < kMG; ++k) y[k] = A.Y + (long long)(k < m.cnt ? m.t[k] : m.t[0]) * A.nw + S.c0;
-  cplx acc[kMG];
-#pragma unroll
-  for (int k = 0; k < kMG; ++k) acc[k] = cmk(0, 0);
-  const int jend = T.b - 1;  // columns < the chunk's last row
-  for (int j0 = 4 * w; j0 < jend; j0 += 32) {
+namespace {
+// sum over columns j = j0, j0+1, j0+2, j0+3, j0 + jstep, ... < jend of L(row, j) v_q[j]
+// for the rows of one lane; get(j) returns the lane's factor entry (0 when the lane
+// has none)
+template <class G>
+__device__ __forceinline__ void col_sweep(const Mem& m, const cplx* const* v, int jfirst, int jstep, int jend,
+                                          G get, cplx* acc) {
+  for (int j0 = jfirst; j0 < jend; j0 += jstep) {
     cplx l[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int j = j0 + u;
-      l[u] = (row && j < i) ? ldf(L + colstart(j, S.n) + (i - j - 1)) : cmk(0, 0);
-    }
-#pragma unroll
-    for (int k = 0; k < kMG; ++k) {
-      if (k >= m.cnt) break;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = j0 + u;
-        if (j < jend) cfma(acc[k], l[u], y[k][j]);
-      }
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < kMG; ++k) part[w][k][lane] = acc[k];
-  __syncthreads();
-  if (w == 0 && row) {
-    for (int k = 0; k < m.cnt; ++k) {
-      cplx s = part[0][k][lane];
-      for (int q = 1; q < 8; ++q) s = cadd(s, part[q][k][lane]);
-      const long long o = (long long)m.t[k] * A.nw + S.c0 + i;
-      A.X[o] = cadd(A.Y[o], s);
-    }
-  }
-}
-
-// forward panel rows: u_k = (children's updates of row k) - sum_j L_kj x_j.
-// CTA per 32-row chunk, lane = row, the 8 warps take interleaved 4-column groups.
-__global__ void __launch_bounds__(256) k3s_fpanel(Solve3Args A, const Task3* tk) {
-  __shared__ cplx part[8][kMG][32];
-  const Mem m = members(A);
-  if (!m.cnt) return;
-  const Task3 T = tk[blockIdx.x];
-  const DSn3 S = A.sn[T.s];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int k = T.a + lane;
-  const bool row = k < T.b;
-  const cplx* L = A.vals + (long long)blockIdx.y * A.nvals + S.pan_off;
-  const cplx* x[kMG];
-#pragma unroll
-  for (int q = 0; q < kMG; ++q) x[q] = A.X + (long long)(q < m.cnt ? m.t[q] : m.t[0]) * A.nw + S.c0;
-  cplx acc[kMG];
-#pragma unroll
-  for (int q = 0; q < kMG; ++q) acc[q] = cmk(0, 0);
-  for (int j0 = 4 * w; j0 < S.n; j0 += 32) {
-    cplx l[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int j = j0 + u;
-      l[u] = (row && j < S.n) ? ldf(L + (long long)j * S.r + k) : cmk(0, 0);
-    }
+    for (int u = 0; u < 4; ++u) l[u] = j0 + u < jend ? get(j0 + u) : cmk(0, 0);
 #pragma unroll
     for (int q = 0; q < kMG; ++q) {
       if (q >= m.cnt) break;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = j0 + u;
-        if (j < S.n) cfma(acc[q], l[u], x[q][j]);
-      }
+      for (int u = 0; u < 4; ++u)
+        if (j0 + u < jend) cfma(acc[q], l[u], v[q][j0 + u]);
     }
   }
+}
+}  // namespace
+
+// forward inverse rows: x_i = y_i + sum_{j<i} Linv_ij y_j (lane = row). CTA tasks:
+// 32 rows, the 8 warps take interleaved 4-column groups, partials combined in warp
+// order; warp tasks: one warp sweeps all columns of its rows.
+__global__ void __launch_bounds__(256) k3s_fdiag(Solve3Args A, const Task3* tk, int nbig) {
+  __shared__ cplx part[8][kMG][32];
+  const Mem m = members(A);
+  if (!m.cnt) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const bool big = int(blockIdx.x) < nbig;
+  const Task3 T = tk[big ? blockIdx.x : nbig + (blockIdx.x - nbig) * 8 + w];
+  if (!big && T.b <= T.a) return;  // padding warp task
+  const int i = T.a + lane;
+  const bool row = i < T.b;
+  const cplx* L = A.vals + (long long)blockIdx.y * A.nvals + T.linv;
+  const cplx* y[kMG];
 #pragma unroll
-  for (int q = 0; q < kMG; ++q) part[w][q][lane] = acc[q];
-  __syncthreads();
-  if (w == 0 && row) {
-    const int m0 = A.cmap0[S.cmap_off + S.n + k], m1 = A.cmap1[S.cmap_off + S.n + k];
-    for (int q = 0; q < m.cnt; ++q) {
+  for (int k = 0; k < kMG; ++k) y[k] = A.Y + (long long)(k < m.cnt ? m.t[k] : m.t[0]) * A.nw + T.c0;
+  cplx acc[kMG];
+#pragma unroll
+  for (int k = 0; k < kMG; ++k) acc[k] = cmk(0, 0);
+  const int n = T.n;
+  auto get = [&](int j) { return (row && j < i) ? ldf(L + colstart(j, n) + (i - j - 1)) : cmk(0, 0); };
+  col_sweep(m, y, big ? 4 * w : 0, big ? 32 : 4, T.b - 1, get, acc);
+  if (big) {
+#pragma unroll
+    for (int k = 0; k < kMG; ++k) part[w][k][lane] = acc[k];
+    __syncthreads();
+    if (w != 0) return;
+#pragma unroll
+    for (int k = 0; k < kMG; ++k) {
+      cplx s = part[0][k][lane];
+      for (int q = 1; q < 8; ++q) s = cadd(s, part[q][k][lane]);
+      acc[k] = s;
+    }
+  }
+  if (!row) return;
+#pragma unroll
+  for (int k = 0; k < kMG; ++k) {
+    if (k >= m.cnt) break;
+    const long long o = (long long)m.t[k] * A.nw + T.c0 + i;
+    A.X[o] = cadd(A.Y[o], acc[k]);
+  }
+}
+
+// forward panel rows: u_k = (children's updates of row k) - sum_j L_kj x_j (lane = row)
+__global__ void __launch_bounds__(256) k3s_fpanel(Solve3Args A, const Task3* tk, int nbig) {
+  __shared__ cplx part[8][kMG][32];
+  const Mem m = members(A);
+  if (!m.cnt) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const bool big = int(blockIdx.x) < nbig;
+  const Task3 T = tk[big ? blockIdx.x : nbig + (blockIdx.x - nbig) * 8 + w];
+  if (!big && T.b <= T.a) return;
+  const int k = T.a + lane;
+  const bool row = k < T.b;
+  const cplx* L = A.vals + (long long)blockIdx.y * A.nvals + T.pan;
+  const cplx* x[kMG];
+#pragma unroll
+  for (int q = 0; q < kMG; ++q) x[q] = A.X + (long long)(q < m.cnt ? m.t[q] : m.t[0]) * A.nw + T.c0;
+  cplx acc[kMG];
+#pragma unroll
+  for (int q = 0; q < kMG; ++q) acc[q] = cmk(0, 0);
+  const int r = T.r;
+  auto get = [&](int j) { return row ? ldf(L + (long long)j * r + k) : cmk(0, 0); };
+  col_sweep(m, x, big ? 4 * w : 0, big ? 32 : 4, T.n, get, acc);
+  if (big) {
+#pragma unroll
+    for (int q = 0; q < kMG; ++q) part[w][q][lane] = acc[q];
+    __syncthreads();
+    if (w != 0) return;
+#pragma unroll
+    for (int q = 0; q < kMG; ++q) {
       cplx s = part[0][q][lane];
       for (int v = 1; v < 8; ++v) s = cadd(s, part[v][q][lane]);
-      cplx* u = A.U + (long long)m.t[q] * A.nupd;
-      cplx c = cmk(0, 0);
-      if (m0 >= 0) c = cadd(c, u[m0]);
-      if (m1 >= 0) c = cadd(c, u[m1]);
-      u[S.upd_off + k] = csub(c, s);
+      acc[q] = s;
     }
+  }
+  if (!row) return;
+  const int m0 = A.cmap0[T.cmap + T.n + k], m1 = A.cmap1[T.cmap + T.n + k];
+#pragma unroll
+  for (int q = 0; q < kMG; ++q) {
+    if (q >= m.cnt) break;
+    cplx* u = A.U + (long long)m.t[q] * A.nupd;
+    cplx c = cmk(0, 0);
+    if (m0 >= 0) c = cadd(c, u[m0]);
+    if (m1 >= 0) c = cadd(c, u[m1]);
+    u[T.upd + k] = csub(c, acc[q]);
   }
 }
 
@@ -447,101 +462,95 @@ __global__ void __launch_bounds__(256) k3s_bgather(Solve3Args A, const Task3* tk
   const Mem m = members(A);
   if (!m.cnt) return;
   const Task3 T = tk[blockIdx.x];
-  const DSn3 S = A.sn[T.s];
   const int k = T.a + threadIdx.x;
   if (k >= T.b) return;
-  const int P = A.rows_all[S.rows_off + k];
+  const int P = A.rows_all[T.rows + k];
   for (int q = 0; q < m.cnt; ++q)
-    A.U[(long long)m.t[q] * A.nupd + S.upd_off + k] = A.X[(long long)m.t[q] * A.nw + P];
+    A.U[(long long)m.t[q] * A.nupd + T.upd + k] = A.X[(long long)m.t[q] * A.nw + P];
 }
 
-// backward panel columns: w_j = z_j / d_j - sum_k L_kj x_rows(k). CTA per 8
-// columns, warp per column, lanes stride the (contiguous) column.
-__global__ void __launch_bounds__(256) k3s_bpanel(Solve3Args A, const Task3* tk) {
+// backward panel columns: w_j = z_j / d_j - sum_k L_kj x_rows(k), lane = column on
+// the row-major copy (coalesced across columns); CTA tasks: 8 warps split the rows
+__global__ void __launch_bounds__(256) k3s_bpanel(Solve3Args A, const Task3* tk, int nbig) {
+  __shared__ cplx part[8][kMG][32];
   const Mem m = members(A);
   if (!m.cnt) return;
-  const Task3 T = tk[blockIdx.x];
-  const DSn3 S = A.sn[T.s];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int j = T.a + w;
-  if (j >= T.b) return;
-  const cplx* vals = A.vals + (long long)blockIdx.y * A.nvals;
-  const cplx* L = vals + S.pan_off + (long long)j * S.r;
+  const bool big = int(blockIdx.x) < nbig;
+  const Task3 T = tk[big ? blockIdx.x : nbig + (blockIdx.x - nbig) * 8 + w];
+  if (!big && T.b <= T.a) return;
+  const int j = T.a + lane;
+  const bool col = j < T.b;
+  const cplx* LT = A.valsT + (long long)blockIdx.y * A.nvals + T.pan;
   const cplx* u[kMG];
 #pragma unroll
-  for (int q = 0; q < kMG; ++q) u[q] = A.U + (long long)(q < m.cnt ? m.t[q] : m.t[0]) * A.nupd + S.upd_off;
-  cplx acc[kMG], acc2[kMG];
+  for (int q = 0; q < kMG; ++q) u[q] = A.U + (long long)(q < m.cnt ? m.t[q] : m.t[0]) * A.nupd + T.upd;
+  cplx acc[kMG];
 #pragma unroll
-  for (int q = 0; q < kMG; ++q) acc[q] = acc2[q] = cmk(0, 0);
-  int k = lane;
-  for (; k + 32 < S.r; k += 64) {
-    const cplx l0 = ldf(L + k), l1 = ldf(L + k + 32);
+  for (int q = 0; q < kMG; ++q) acc[q] = cmk(0, 0);
+  const int n = T.n;
+  auto get = [&](int k) { return col ? ldf(LT + (long long)k * n + j) : cmk(0, 0); };
+  col_sweep(m, u, big ? 4 * w : 0, big ? 32 : 4, T.r, get, acc);
+  if (big) {
 #pragma unroll
-    for (int q = 0; q < kMG; ++q) {
-      if (q >= m.cnt) break;
-      cfma(acc[q], l0, u[q][k]);
-      cfma(acc2[q], l1, u[q][k + 32]);
-    }
-  }
-  if (k < S.r) {
-    const cplx l0 = ldf(L + k);
+    for (int q = 0; q < kMG; ++q) part[w][q][lane] = acc[q];
+    __syncthreads();
+    if (w != 0) return;
 #pragma unroll
     for (int q = 0; q < kMG; ++q) {
-      if (q >= m.cnt) break;
-      cfma(acc[q], l0, u[q][k]);
+      cplx s = part[0][q][lane];
+      for (int v = 1; v < 8; ++v) s = cadd(s, part[v][q][lane]);
+      acc[q] = s;
     }
   }
-  const cplx d = vals[S.c0 + j];
+  if (!col) return;
+  const cplx d = A.vals[(long long)blockIdx.y * A.nvals + T.c0 + j];
 #pragma unroll
   for (int q = 0; q < kMG; ++q) {
     if (q >= m.cnt) break;
-    const cplx s = warp_sum(cadd(acc[q], acc2[q]));
-    if (lane == 0) {
-      const long long o = (long long)m.t[q] * A.nw + S.c0 + j;
-      A.Y[o] = csub(cdiv(A.X[o], d), s);
-    }
+    const long long o = (long long)m.t[q] * A.nw + T.c0 + j;
+    A.Y[o] = csub(cdiv(A.X[o], d), acc[q]);
   }
 }
 
-// backward inverse columns: x_j = w_j + sum_{i>j} Linv_ij w_i (warp per column)
-__global__ void __launch_bounds__(256) k3s_bdiag(Solve3Args A, const Task3* tk) {
+// backward inverse columns: x_j = w_j + sum_{i>j} Linv_ij w_i, lane = column on the
+// row-major packed copy; CTA tasks: 8 warps split the rows
+__global__ void __launch_bounds__(256) k3s_bdiag(Solve3Args A, const Task3* tk, int nbig) {
+  __shared__ cplx part[8][kMG][32];
   const Mem m = members(A);
   if (!m.cnt) return;
-  const Task3 T = tk[blockIdx.x];
-  const DSn3 S = A.sn[T.s];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int j = T.a + w;
-  if (j >= T.b) return;
-  const cplx* L = A.vals + (long long)blockIdx.y * A.nvals + S.linv_off + colstart(j, S.n) - (j + 1);
+  const bool big = int(blockIdx.x) < nbig;
+  const Task3 T = tk[big ? blockIdx.x : nbig + (blockIdx.x - nbig) * 8 + w];
+  if (!big && T.b <= T.a) return;
+  const int j = T.a + lane;
+  const bool col = j < T.b;
+  const cplx* LT = A.valsT + (long long)blockIdx.y * A.nvals + T.linv;
   const cplx* y[kMG];
 #pragma unroll
-  for (int q = 0; q < kMG; ++q) y[q] = A.Y + (long long)(q < m.cnt ? m.t[q] : m.t[0]) * A.nw + S.c0;
-  cplx acc[kMG], acc2[kMG];
+  for (int q = 0; q < kMG; ++q) y[q] = A.Y + (long long)(q < m.cnt ? m.t[q] : m.t[0]) * A.nw + T.c0;
+  cplx acc[kMG];
 #pragma unroll
-  for (int q = 0; q < kMG; ++q) acc[q] = acc2[q] = cmk(0, 0);
-  int i = j + 1 + lane;
-  for (; i + 32 < S.n; i += 64) {
-    const cplx l0 = ldf(L + i), l1 = ldf(L + i + 32);
+  for (int q = 0; q < kMG; ++q) acc[q] = cmk(0, 0);
+  auto get = [&](int i) { return (col && i > j) ? ldf(LT + (long long)i * (i - 1) / 2 + j) : cmk(0, 0); };
+  col_sweep(m, y, T.a + 1 + (big ? 4 * w : 0), big ? 32 : 4, T.n, get, acc);
+  if (big) {
 #pragma unroll
-    for (int q = 0; q < kMG; ++q) {
-      if (q >= m.cnt) break;
-      cfma(acc[q], l0, y[q][i]);
-      cfma(acc2[q], l1, y[q][i + 32]);
-    }
-  }
-  if (i < S.n) {
-    const cplx l0 = ldf(L + i);
+    for (int q = 0; q < kMG; ++q) part[w][q][lane] = acc[q];
+    __syncthreads();
+    if (w != 0) return;
 #pragma unroll
     for (int q = 0; q < kMG; ++q) {
-      if (q >= m.cnt) break;
-      cfma(acc[q], l0, y[q][i]);
+      cplx s = part[0][q][lane];
+      for (int v = 1; v < 8; ++v) s = cadd(s, part[v][q][lane]);
+      acc[q] = s;
     }
   }
+  if (!col) return;
 #pragma unroll
   for (int q = 0; q < kMG; ++q) {
     if (q >= m.cnt) break;
-    const cplx s = warp_sum(cadd(acc[q], acc2[q]));
-    if (lane == 0) A.X[(long long)m.t[q] * A.nw + S.c0 + j] = cadd(y[q][j], s);
+    A.X[(long long)m.t[q] * A.nw + T.c0 + j] = cadd(y[q][j], acc[q]);
   }
 }
 
@@ -551,20 +560,20 @@ void s3_ring(const Solve3Args& A, int ncls, int ng, cudaStream_t st) {
 void s3_fasm(const Solve3Args& A, const Task3* t, int nt, int ncls, int ng, cudaStream_t st) {
   if (nt) k3s_fasm<<<dim3(nt, ncls, ng), 256, 0, st>>>(A, t);
 }
-void s3_fdiag(const Solve3Args& A, const Task3* t, int nt, int ncls, int ng, cudaStream_t st) {
-  if (nt) k3s_fdiag<<<dim3(nt, ncls, ng), 256, 0, st>>>(A, t);
+void s3_fdiag(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ng, cudaStream_t st) {
+  if (nt) k3s_fdiag<<<dim3(nbig + (nt - nbig + 7) / 8, ncls, ng), 256, 0, st>>>(A, t, nbig);
 }
-void s3_fpanel(const Solve3Args& A, const Task3* t, int nt, int ncls, int ng, cudaStream_t st) {
-  if (nt) k3s_fpanel<<<dim3(nt, ncls, ng), 256, 0, st>>>(A, t);
+void s3_fpanel(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ng, cudaStream_t st) {
+  if (nt) k3s_fpanel<<<dim3(nbig + (nt - nbig + 7) / 8, ncls, ng), 256, 0, st>>>(A, t, nbig);
 }
 void s3_bgather(const Solve3Args& A, const Task3* t, int nt, int ncls, int ng, cudaStream_t st) {
   if (nt) k3s_bgather<<<dim3(nt, ncls, ng), 256, 0, st>>>(A, t);
 }
-void s3_bpanel(const Solve3Args& A, const Task3* t, int nt, int ncls, int ng, cudaStream_t st) {
-  if (nt) k3s_bpanel<<<dim3(nt, ncls, ng), 256, 0, st>>>(A, t);
+void s3_bpanel(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ng, cudaStream_t st) {
+  if (nt) k3s_bpanel<<<dim3(nbig + (nt - nbig + 7) / 8, ncls, ng), 256, 0, st>>>(A, t, nbig);
 }
-void s3_bdiag(const Solve3Args& A, const Task3* t, int nt, int ncls, int ng, cudaStream_t st) {
-  if (nt) k3s_bdiag<<<dim3(nt, ncls, ng), 256, 0, st>>>(A, t);
+void s3_bdiag(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ng, cudaStream_t st) {
+  if (nt) k3s_bdiag<<<dim3(nbig + (nt - nbig + 7) / 8, ncls, ng), 256, 0, st>>>(A, t, nbig);
 }
 
 // ================================================================ DDM step

@@ -15,9 +15,12 @@ struct DSn3 {
   int aent0, aent1;
 };
 
-// a piece of a supernode's work: rows / columns [a, b)
+// a piece of a supernode's work: rows / columns [a, b), with the supernode's
+// offsets carried along (one load per task)
 struct Task3 {
   int s, a, b, pad;
+  int c0, n, r, pad2;
+  long long linv, pan, upd, cmap, rows, pad3;
 };
 
 // ------------------------------------------------------------ factorization
@@ -31,6 +34,7 @@ struct Fac3Args {
   long long naent;
   const int* ext;
   cplx* vals;            // factor values, per class stride nvals
+  cplx* valsT;           // the same blocks transposed (row-major) for the backward sweep
   long long nvals;
   int cls0;              // first class of the batch
 };
@@ -49,7 +53,8 @@ void f3_extract(const Fac3Args& F, const int* lv, int nlv, int nb, long long max
 // B + t * nw (factor order); its forward/backward update vector at U + t * nupd.
 struct Solve3Args {
   const DSn3* sn;
-  const cplx* vals;
+  const cplx* vals;   // forward layout: inverse blocks and panels column major
+  const cplx* valsT;  // backward layout: the same blocks row major
   long long nvals;
   const int* rows_all;
   const int* cmap0;
@@ -67,13 +72,15 @@ struct Solve3Args {
 };
 constexpr int kMG = 4;  // right-hand sides per CTA pass (member group)
 
+// fdiag / fpanel: the first nbig tasks are CTA tasks (8 warps split the columns of
+// 32 rows), the rest warp tasks (8 per CTA: supernodes with few columns)
 void s3_ring(const Solve3Args& A, int ncls, int ngroups, cudaStream_t st);
 void s3_fasm(const Solve3Args& A, const Task3* t, int nt, int ncls, int ngroups, cudaStream_t st);
-void s3_fdiag(const Solve3Args& A, const Task3* t, int nt, int ncls, int ngroups, cudaStream_t st);
-void s3_fpanel(const Solve3Args& A, const Task3* t, int nt, int ncls, int ngroups, cudaStream_t st);
+void s3_fdiag(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ngroups, cudaStream_t st);
+void s3_fpanel(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ngroups, cudaStream_t st);
 void s3_bgather(const Solve3Args& A, const Task3* t, int nt, int ncls, int ngroups, cudaStream_t st);
-void s3_bpanel(const Solve3Args& A, const Task3* t, int nt, int ncls, int ngroups, cudaStream_t st);
-void s3_bdiag(const Solve3Args& A, const Task3* t, int nt, int ncls, int ngroups, cudaStream_t st);
+void s3_bpanel(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ngroups, cudaStream_t st);
+void s3_bdiag(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ngroups, cudaStream_t st);
 
 // ------------------------------------------------------------------ DDM step
 struct Sub3Dev {
