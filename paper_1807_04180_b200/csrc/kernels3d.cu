@@ -6,6 +6,7 @@
 // oracle/hddm_oracle3.c (the reference has no 3-D code); every output has one
 // writer and a fixed summation order, so results are deterministic.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "kernels3d.cuh"
@@ -230,6 +231,110 @@ __global__ void __launch_bounds__(256) k3f_update(Fac3Args F, const int* lv, int
   }
 }
 
+// The same trailing update on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64):
+// these fronts are genuinely dense contractions (north_star item 1). Complex
+// products as four real MMAs: Cr += Wr Lr^T - Wi Li^T, Ci += Wr Li^T + Wi Lr^T.
+// CTA tile 64 x 64, 8 warps of 32 x 16 (4 x 2 blocks of 8 x 8), K = the panel
+// width in steps of 4; shared-memory rows padded to 66 so the fragment loads of a
+// quarter warp hit distinct banks.
+constexpr int kTileP = kTile + 2;
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+__global__ void __launch_bounds__(256) k3f_update_mma(Fac3Args F, const int* lv, int k0) {
+  extern __shared__ __align__(16) unsigned char smem3[];
+  cplx (*As)[kTileP] = reinterpret_cast<cplx (*)[kTileP]>(smem3);
+  cplx (*Bs)[kTileP] = reinterpret_cast<cplx (*)[kTileP]>(smem3 + sizeof(cplx) * kNB * kTileP);
+  const DSn3 S = F.sn[lv[blockIdx.y]];
+  if (S.n <= k0) return;
+  const int b = min(kNB, S.n - k0);
+  const int t0 = k0 + b;
+  const int M = S.n + S.r - t0;
+  const int T = (M + kTile - 1) / kTile;
+  const long long nmain = (long long)T * (T + 1) / 2;
+  const int ne = min(S.n, t0);
+  const int TE = (ne + kTile - 1) / kTile;
+  const int TC = S.n > t0 ? (S.n - t0 + kTile - 1) / kTile : 0;
+  const long long tid = blockIdx.x;
+  long long rbase, cbase;
+  int rlim, clim;
+  if (tid < nmain) {
+    int ti = int((sqrt(8.0 * double(tid) + 1.0) - 1.0) * 0.5);
+    while ((long long)(ti + 1) * (ti + 2) / 2 <= tid) ++ti;
+    while ((long long)ti * (ti + 1) / 2 > tid) --ti;
+    const int tj = int(tid - (long long)ti * (ti + 1) / 2);
+    rbase = t0 + ti * kTile;
+    cbase = t0 + tj * kTile;
+    rlim = min(kTile, S.n + S.r - int(rbase));
+    clim = min(kTile, S.n + S.r - int(cbase));
+  } else if (tid < nmain + (long long)TE * TC) {
+    const long long u = tid - nmain;
+    const int te = int(u / TC), tc = int(u % TC);
+    rbase = S.n + S.r + te * kTile;
+    cbase = t0 + tc * kTile;
+    rlim = min(kTile, ne - te * kTile);
+    clim = min(kTile, S.n - (t0 + tc * kTile));
+  } else {
+    return;
+  }
+  cplx* fr = F.fronts + blockIdx.z * F.fw + S.front_off;
+  const long long ld = 2LL * S.n + S.r;
+  for (int e = threadIdx.x; e < kNB * kTile; e += blockDim.x) {
+    const int i = e % kTile, c = e / kTile;
+    cplx a = cmk(0, 0), bb = cmk(0, 0);
+    if (c < b) {
+      const cplx* col = fr + (long long)(k0 + c) * ld;
+      const cplx d = col[k0 + c];
+      if (i < rlim) a = cmul(col[rbase + i], d);
+      if (i < clim) bb = col[cbase + i];
+    }
+    As[c][i] = a;
+    Bs[c][i] = bb;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int r0 = (w >> 2) * 32, c0 = (w & 3) * 16;
+  const int g = lane >> 2, q = lane & 3;
+  double cr[4][2][2], ci[4][2][2];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 2; ++v) cr[u][v][0] = cr[u][v][1] = ci[u][v][0] = ci[u][v][1] = 0.0;
+  const int ksteps = (b + 3) / 4;
+  for (int kk = 0; kk < ksteps; ++kk) {
+    const int c = kk * 4 + q;
+    cplx a[4], l[2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = As[c][r0 + u * 8 + g];
+#pragma unroll
+    for (int v = 0; v < 2; ++v) l[v] = Bs[c][c0 + v * 8 + g];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        dmma(cr[u][v][0], cr[u][v][1], a[u].x, l[v].x);
+        dmma(cr[u][v][0], cr[u][v][1], -a[u].y, l[v].y);
+        dmma(ci[u][v][0], ci[u][v][1], a[u].x, l[v].y);
+        dmma(ci[u][v][0], ci[u][v][1], a[u].y, l[v].x);
+      }
+  }
+#pragma unroll
+  for (int v = 0; v < 2; ++v)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = c0 + v * 8 + q * 2 + h;
+      if (j >= clim) continue;
+      cplx* col = fr + (cbase + j) * ld + rbase;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = r0 + u * 8 + g;
+        if (i < rlim) col[i] = csub(col[i], cmk(cr[u][v][h], ci[u][v][h]));
+      }
+    }
+}
+
 // factor values of the finished fronts: D, the packed inverse of the unit-lower
 // diagonal block (Linv_ij = L_E(j, i) d_i), the panel (column major)
 __global__ void __launch_bounds__(256) k3f_extract(Fac3Args F, const int* lv) {
@@ -277,13 +382,21 @@ void f3_trsm(const Fac3Args& F, const int* lv, int nlv, int nb, int k0, int maxr
 }
 void f3_update(const Fac3Args& F, const int* lv, int nlv, int nb, int k0, long long maxtiles,
                cudaStream_t st) {
+  // DMMA by default; HDDM3_FACTOR_FMA=1 selects the CUDA-core kernel (same math)
+  static const bool fma = std::getenv("HDDM3_FACTOR_FMA") != nullptr;
   constexpr size_t smem = 2 * sizeof(cplx) * kNB * kTile;
+  constexpr size_t smemp = 2 * sizeof(cplx) * kNB * kTileP;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k3f_update, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k3f_update_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemp));
     attr = true;
   }
-  if (nlv && maxtiles > 0) k3f_update<<<dim3(unsigned(maxtiles), nlv, nb), 256, smem, st>>>(F, lv, k0);
+  if (!(nlv && maxtiles > 0)) return;
+  if (fma)
+    k3f_update<<<dim3(unsigned(maxtiles), nlv, nb), 256, smem, st>>>(F, lv, k0);
+  else
+    k3f_update_mma<<<dim3(unsigned(maxtiles), nlv, nb), 256, smemp, st>>>(F, lv, k0);
 }
 void f3_extract(const Fac3Args& F, const int* lv, int nlv, int nb, long long maxent, cudaStream_t st) {
   if (!nlv) return;
