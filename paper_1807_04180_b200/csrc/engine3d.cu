@@ -59,7 +59,7 @@ struct hddm3_engine {
   int dev = -1;
   cudaStream_t st = nullptr, st2 = nullptr;
   std::string err;
-  int nsub = 0, ncls = 0, nw = 0, ngroups = 1, max_members = 1;
+  int nsub = 0, ncls = 0, nw = 0, ngroups = 1, max_members = 1, mg = 4;
   long long ng = 0;
   double factor_ms = 0;
   std::vector<double> probe;
@@ -214,7 +214,8 @@ void hddm3_engine::create(const hddm3_problem& p) {
   build_sym3(S.subs[0].nn[0], S.subs[0].nn[1], S.subs[0].nn[2], Y);
   nw = Y.n;
   for (int c = 0; c < ncls; ++c) max_members = std::max(max_members, S.cls_ptr[c + 1] - S.cls_ptr[c]);
-  ngroups = (max_members + kMG - 1) / kMG;
+  mg = max_members == 1 ? 1 : kMG;
+  ngroups = (max_members + mg - 1) / mg;
 
   // symbolic tables
   std::vector<DSn3> sn(Y.sn.size());
@@ -571,6 +572,7 @@ Solve3Args hddm3_engine::solve_args(const cplx* B, cplx* X, const int* flag, int
   A.cls_mem = d_cls_mem;
   A.flag = flag;
   A.flag_on = on;
+  A.mg = mg;
   return A;
 }
 

@@ -406,20 +406,22 @@ void f3_extract(const Fac3Args& F, const int* lv, int nlv, int nb, long long max
 
 // ================================================================ solves
 // Grid: (task, class, member group). The members of class c in group g are
-// cls_mem[cls_ptr[c] + g*kMG + k], k < kMG; a member takes part iff its flag says so.
+// cls_mem[cls_ptr[c] + g*MG + k], k < MG; a member takes part iff its flag says so.
 namespace {
+template <int MG>
 struct Mem {
-  int t[kMG];
+  int t[MG];
   int cnt;
 };
-__device__ __forceinline__ Mem members(const Solve3Args& A) {
-  Mem m;
+template <int MG>
+__device__ __forceinline__ Mem<MG> members(const Solve3Args& A) {
+  Mem<MG> m;
   const int c = blockIdx.y, g = blockIdx.z;
   const int p0 = A.cls_ptr[c], p1 = A.cls_ptr[c + 1];
   m.cnt = 0;
 #pragma unroll
-  for (int k = 0; k < kMG; ++k) {
-    const int q = p0 + g * kMG + k;
+  for (int k = 0; k < MG; ++k) {
+    const int q = p0 + g * MG + k;
     m.t[k] = -1;
     if (q < p1) {
       const int t = A.cls_mem[q];
@@ -431,8 +433,9 @@ __device__ __forceinline__ Mem members(const Solve3Args& A) {
 }  // namespace
 
 // shell (identity rows): x = b
-__global__ void __launch_bounds__(256) k3s_ring(Solve3Args A) {
-  const Mem m = members(A);
+template <int MG>
+__global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_ring(Solve3Args A) {
+  const Mem<MG> m = members<MG>(A);
   for (int k = 0; k < m.cnt; ++k) {
     const long long o = (long long)m.t[k] * A.nw;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.nshell; i += gridDim.x * blockDim.x)
@@ -441,8 +444,9 @@ __global__ void __launch_bounds__(256) k3s_ring(Solve3Args A) {
 }
 
 // forward assembly of the own entries: Y = b + the children's update vectors
-__global__ void __launch_bounds__(256) k3s_fasm(Solve3Args A, const Task3* tk) {
-  const Mem m = members(A);
+template <int MG>
+__global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_fasm(Solve3Args A, const Task3* tk) {
+  const Mem<MG> m = members<MG>(A);
   if (!m.cnt) return;
   const Task3 T = tk[blockIdx.x];
   const int i = T.a + threadIdx.x;
@@ -462,15 +466,15 @@ namespace {
 // sum over columns j = j0, j0+1, j0+2, j0+3, j0 + jstep, ... < jend of L(row, j) v_q[j]
 // for the rows of one lane; get(j) returns the lane's factor entry (0 when the lane
 // has none)
-template <class G>
-__device__ __forceinline__ void col_sweep(const Mem& m, const cplx* const* v, int jfirst, int jstep, int jend,
+template <int MG, class G>
+__device__ __forceinline__ void col_sweep(const Mem<MG>& m, const cplx* const* v, int jfirst, int jstep, int jend,
                                           G get, cplx* acc) {
   for (int j0 = jfirst; j0 < jend; j0 += jstep) {
     cplx l[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) l[u] = j0 + u < jend ? get(j0 + u) : cmk(0, 0);
 #pragma unroll
-    for (int q = 0; q < kMG; ++q) {
+    for (int q = 0; q < MG; ++q) {
       if (q >= m.cnt) break;
 #pragma unroll
       for (int u = 0; u < 4; ++u)
@@ -483,9 +487,10 @@ __device__ __forceinline__ void col_sweep(const Mem& m, const cplx* const* v, in
 // forward inverse rows: x_i = y_i + sum_{j<i} Linv_ij y_j (lane = row). CTA tasks:
 // 32 rows, the 8 warps take interleaved 4-column groups, partials combined in warp
 // order; warp tasks: one warp sweeps all columns of its rows.
-__global__ void __launch_bounds__(256) k3s_fdiag(Solve3Args A, const Task3* tk, int nbig) {
-  __shared__ cplx part[8][kMG][32];
-  const Mem m = members(A);
+template <int MG>
+__global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_fdiag(Solve3Args A, const Task3* tk, int nbig) {
+  __shared__ cplx part[8][MG][32];
+  const Mem<MG> m = members<MG>(A);
   if (!m.cnt) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const bool big = int(blockIdx.x) < nbig;
@@ -494,22 +499,22 @@ __global__ void __launch_bounds__(256) k3s_fdiag(Solve3Args A, const Task3* tk, 
   const int i = T.a + lane;
   const bool row = i < T.b;
   const cplx* L = A.vals + (long long)blockIdx.y * A.nvals + T.linv;
-  const cplx* y[kMG];
+  const cplx* y[MG];
 #pragma unroll
-  for (int k = 0; k < kMG; ++k) y[k] = A.Y + (long long)(k < m.cnt ? m.t[k] : m.t[0]) * A.nw + T.c0;
-  cplx acc[kMG];
+  for (int k = 0; k < MG; ++k) y[k] = A.Y + (long long)(k < m.cnt ? m.t[k] : m.t[0]) * A.nw + T.c0;
+  cplx acc[MG];
 #pragma unroll
-  for (int k = 0; k < kMG; ++k) acc[k] = cmk(0, 0);
+  for (int k = 0; k < MG; ++k) acc[k] = cmk(0, 0);
   const int n = T.n;
   auto get = [&](int j) { return (row && j < i) ? ldf(L + colstart(j, n) + (i - j - 1)) : cmk(0, 0); };
   col_sweep(m, y, big ? 4 * w : 0, big ? 32 : 4, T.b - 1, get, acc);
   if (big) {
 #pragma unroll
-    for (int k = 0; k < kMG; ++k) part[w][k][lane] = acc[k];
+    for (int k = 0; k < MG; ++k) part[w][k][lane] = acc[k];
     __syncthreads();
     if (w != 0) return;
 #pragma unroll
-    for (int k = 0; k < kMG; ++k) {
+    for (int k = 0; k < MG; ++k) {
       cplx s = part[0][k][lane];
       for (int q = 1; q < 8; ++q) s = cadd(s, part[q][k][lane]);
       acc[k] = s;
@@ -517,7 +522,7 @@ __global__ void __launch_bounds__(256) k3s_fdiag(Solve3Args A, const Task3* tk, 
   }
   if (!row) return;
 #pragma unroll
-  for (int k = 0; k < kMG; ++k) {
+  for (int k = 0; k < MG; ++k) {
     if (k >= m.cnt) break;
     const long long o = (long long)m.t[k] * A.nw + T.c0 + i;
     A.X[o] = cadd(A.Y[o], acc[k]);
@@ -525,9 +530,10 @@ __global__ void __launch_bounds__(256) k3s_fdiag(Solve3Args A, const Task3* tk, 
 }
 
 // forward panel rows: u_k = (children's updates of row k) - sum_j L_kj x_j (lane = row)
-__global__ void __launch_bounds__(256) k3s_fpanel(Solve3Args A, const Task3* tk, int nbig) {
-  __shared__ cplx part[8][kMG][32];
-  const Mem m = members(A);
+template <int MG>
+__global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_fpanel(Solve3Args A, const Task3* tk, int nbig) {
+  __shared__ cplx part[8][MG][32];
+  const Mem<MG> m = members<MG>(A);
   if (!m.cnt) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const bool big = int(blockIdx.x) < nbig;
@@ -536,22 +542,22 @@ __global__ void __launch_bounds__(256) k3s_fpanel(Solve3Args A, const Task3* tk,
   const int k = T.a + lane;
   const bool row = k < T.b;
   const cplx* L = A.vals + (long long)blockIdx.y * A.nvals + T.pan;
-  const cplx* x[kMG];
+  const cplx* x[MG];
 #pragma unroll
-  for (int q = 0; q < kMG; ++q) x[q] = A.X + (long long)(q < m.cnt ? m.t[q] : m.t[0]) * A.nw + T.c0;
-  cplx acc[kMG];
+  for (int q = 0; q < MG; ++q) x[q] = A.X + (long long)(q < m.cnt ? m.t[q] : m.t[0]) * A.nw + T.c0;
+  cplx acc[MG];
 #pragma unroll
-  for (int q = 0; q < kMG; ++q) acc[q] = cmk(0, 0);
+  for (int q = 0; q < MG; ++q) acc[q] = cmk(0, 0);
   const int r = T.r;
   auto get = [&](int j) { return row ? ldf(L + (long long)j * r + k) : cmk(0, 0); };
   col_sweep(m, x, big ? 4 * w : 0, big ? 32 : 4, T.n, get, acc);
   if (big) {
 #pragma unroll
-    for (int q = 0; q < kMG; ++q) part[w][q][lane] = acc[q];
+    for (int q = 0; q < MG; ++q) part[w][q][lane] = acc[q];
     __syncthreads();
     if (w != 0) return;
 #pragma unroll
-    for (int q = 0; q < kMG; ++q) {
+    for (int q = 0; q < MG; ++q) {
       cplx s = part[0][q][lane];
       for (int v = 1; v < 8; ++v) s = cadd(s, part[v][q][lane]);
       acc[q] = s;
@@ -560,7 +566,7 @@ __global__ void __launch_bounds__(256) k3s_fpanel(Solve3Args A, const Task3* tk,
   if (!row) return;
   const int m0 = A.cmap0[T.cmap + T.n + k], m1 = A.cmap1[T.cmap + T.n + k];
 #pragma unroll
-  for (int q = 0; q < kMG; ++q) {
+  for (int q = 0; q < MG; ++q) {
     if (q >= m.cnt) break;
     cplx* u = A.U + (long long)m.t[q] * A.nupd;
     cplx c = cmk(0, 0);
@@ -571,8 +577,9 @@ __global__ void __launch_bounds__(256) k3s_fpanel(Solve3Args A, const Task3* tk,
 }
 
 // backward gather of the ancestors' solution at the supernode's rows into U
-__global__ void __launch_bounds__(256) k3s_bgather(Solve3Args A, const Task3* tk) {
-  const Mem m = members(A);
+template <int MG>
+__global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_bgather(Solve3Args A, const Task3* tk) {
+  const Mem<MG> m = members<MG>(A);
   if (!m.cnt) return;
   const Task3 T = tk[blockIdx.x];
   const int k = T.a + threadIdx.x;
@@ -584,9 +591,10 @@ __global__ void __launch_bounds__(256) k3s_bgather(Solve3Args A, const Task3* tk
 
 // backward panel columns: w_j = z_j / d_j - sum_k L_kj x_rows(k), lane = column on
 // the row-major copy (coalesced across columns); CTA tasks: 8 warps split the rows
-__global__ void __launch_bounds__(256) k3s_bpanel(Solve3Args A, const Task3* tk, int nbig) {
-  __shared__ cplx part[8][kMG][32];
-  const Mem m = members(A);
+template <int MG>
+__global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_bpanel(Solve3Args A, const Task3* tk, int nbig) {
+  __shared__ cplx part[8][MG][32];
+  const Mem<MG> m = members<MG>(A);
   if (!m.cnt) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const bool big = int(blockIdx.x) < nbig;
@@ -595,22 +603,22 @@ __global__ void __launch_bounds__(256) k3s_bpanel(Solve3Args A, const Task3* tk,
   const int j = T.a + lane;
   const bool col = j < T.b;
   const cplx* LT = A.valsT + (long long)blockIdx.y * A.nvals + T.pan;
-  const cplx* u[kMG];
+  const cplx* u[MG];
 #pragma unroll
-  for (int q = 0; q < kMG; ++q) u[q] = A.U + (long long)(q < m.cnt ? m.t[q] : m.t[0]) * A.nupd + T.upd;
-  cplx acc[kMG];
+  for (int q = 0; q < MG; ++q) u[q] = A.U + (long long)(q < m.cnt ? m.t[q] : m.t[0]) * A.nupd + T.upd;
+  cplx acc[MG];
 #pragma unroll
-  for (int q = 0; q < kMG; ++q) acc[q] = cmk(0, 0);
+  for (int q = 0; q < MG; ++q) acc[q] = cmk(0, 0);
   const int n = T.n;
   auto get = [&](int k) { return col ? ldf(LT + (long long)k * n + j) : cmk(0, 0); };
   col_sweep(m, u, big ? 4 * w : 0, big ? 32 : 4, T.r, get, acc);
   if (big) {
 #pragma unroll
-    for (int q = 0; q < kMG; ++q) part[w][q][lane] = acc[q];
+    for (int q = 0; q < MG; ++q) part[w][q][lane] = acc[q];
     __syncthreads();
     if (w != 0) return;
 #pragma unroll
-    for (int q = 0; q < kMG; ++q) {
+    for (int q = 0; q < MG; ++q) {
       cplx s = part[0][q][lane];
       for (int v = 1; v < 8; ++v) s = cadd(s, part[v][q][lane]);
       acc[q] = s;
@@ -619,7 +627,7 @@ __global__ void __launch_bounds__(256) k3s_bpanel(Solve3Args A, const Task3* tk,
   if (!col) return;
   const cplx d = A.vals[(long long)blockIdx.y * A.nvals + T.c0 + j];
 #pragma unroll
-  for (int q = 0; q < kMG; ++q) {
+  for (int q = 0; q < MG; ++q) {
     if (q >= m.cnt) break;
     const long long o = (long long)m.t[q] * A.nw + T.c0 + j;
     A.Y[o] = csub(cdiv(A.X[o], d), acc[q]);
@@ -628,9 +636,10 @@ __global__ void __launch_bounds__(256) k3s_bpanel(Solve3Args A, const Task3* tk,
 
 // backward inverse columns: x_j = w_j + sum_{i>j} Linv_ij w_i, lane = column on the
 // row-major packed copy; CTA tasks: 8 warps split the rows
-__global__ void __launch_bounds__(256) k3s_bdiag(Solve3Args A, const Task3* tk, int nbig) {
-  __shared__ cplx part[8][kMG][32];
-  const Mem m = members(A);
+template <int MG>
+__global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_bdiag(Solve3Args A, const Task3* tk, int nbig) {
+  __shared__ cplx part[8][MG][32];
+  const Mem<MG> m = members<MG>(A);
   if (!m.cnt) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const bool big = int(blockIdx.x) < nbig;
@@ -639,21 +648,21 @@ __global__ void __launch_bounds__(256) k3s_bdiag(Solve3Args A, const Task3* tk, 
   const int j = T.a + lane;
   const bool col = j < T.b;
   const cplx* LT = A.valsT + (long long)blockIdx.y * A.nvals + T.linv;
-  const cplx* y[kMG];
+  const cplx* y[MG];
 #pragma unroll
-  for (int q = 0; q < kMG; ++q) y[q] = A.Y + (long long)(q < m.cnt ? m.t[q] : m.t[0]) * A.nw + T.c0;
-  cplx acc[kMG];
+  for (int q = 0; q < MG; ++q) y[q] = A.Y + (long long)(q < m.cnt ? m.t[q] : m.t[0]) * A.nw + T.c0;
+  cplx acc[MG];
 #pragma unroll
-  for (int q = 0; q < kMG; ++q) acc[q] = cmk(0, 0);
+  for (int q = 0; q < MG; ++q) acc[q] = cmk(0, 0);
   auto get = [&](int i) { return (col && i > j) ? ldf(LT + (long long)i * (i - 1) / 2 + j) : cmk(0, 0); };
   col_sweep(m, y, T.a + 1 + (big ? 4 * w : 0), big ? 32 : 4, T.n, get, acc);
   if (big) {
 #pragma unroll
-    for (int q = 0; q < kMG; ++q) part[w][q][lane] = acc[q];
+    for (int q = 0; q < MG; ++q) part[w][q][lane] = acc[q];
     __syncthreads();
     if (w != 0) return;
 #pragma unroll
-    for (int q = 0; q < kMG; ++q) {
+    for (int q = 0; q < MG; ++q) {
       cplx s = part[0][q][lane];
       for (int v = 1; v < 8; ++v) s = cadd(s, part[v][q][lane]);
       acc[q] = s;
@@ -661,33 +670,63 @@ __global__ void __launch_bounds__(256) k3s_bdiag(Solve3Args A, const Task3* tk, 
   }
   if (!col) return;
 #pragma unroll
-  for (int q = 0; q < kMG; ++q) {
+  for (int q = 0; q < MG; ++q) {
     if (q >= m.cnt) break;
     A.X[(long long)m.t[q] * A.nw + T.c0 + j] = cadd(y[q][j], acc[q]);
   }
 }
 
+template <int MG>
+static void s3t_ring(const Solve3Args& A, int ncls, int ng, cudaStream_t st) {
+  k3s_ring<MG><<<dim3(std::max(1, std::min(64, (A.nshell + 255) / 256)), ncls, ng), 256, 0, st>>>(A);
+}
+template <int MG>
+static void s3t_fasm(const Solve3Args& A, const Task3* t, int nt, int ncls, int ng, cudaStream_t st) {
+  if (nt) k3s_fasm<MG><<<dim3(nt, ncls, ng), 256, 0, st>>>(A, t);
+}
+template <int MG>
+static void s3t_fdiag(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ng, cudaStream_t st) {
+  if (nt) k3s_fdiag<MG><<<dim3(nbig + (nt - nbig + 7) / 8, ncls, ng), 256, 0, st>>>(A, t, nbig);
+}
+template <int MG>
+static void s3t_fpanel(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ng, cudaStream_t st) {
+  if (nt) k3s_fpanel<MG><<<dim3(nbig + (nt - nbig + 7) / 8, ncls, ng), 256, 0, st>>>(A, t, nbig);
+}
+template <int MG>
+static void s3t_bgather(const Solve3Args& A, const Task3* t, int nt, int ncls, int ng, cudaStream_t st) {
+  if (nt) k3s_bgather<MG><<<dim3(nt, ncls, ng), 256, 0, st>>>(A, t);
+}
+template <int MG>
+static void s3t_bpanel(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ng, cudaStream_t st) {
+  if (nt) k3s_bpanel<MG><<<dim3(nbig + (nt - nbig + 7) / 8, ncls, ng), 256, 0, st>>>(A, t, nbig);
+}
+template <int MG>
+static void s3t_bdiag(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ng, cudaStream_t st) {
+  if (nt) k3s_bdiag<MG><<<dim3(nbig + (nt - nbig + 7) / 8, ncls, ng), 256, 0, st>>>(A, t, nbig);
+}
+
+
+// member groups of 4 right-hand sides, or 1 when every class has one member (config 5:
+// fewer registers, 4 CTAs per SM)
 void s3_ring(const Solve3Args& A, int ncls, int ng, cudaStream_t st) {
-  k3s_ring<<<dim3(std::max(1, std::min(64, (A.nshell + 255) / 256)), ncls, ng), 256, 0, st>>>(A);
+  if (A.mg == 1) s3t_ring<1>(A, ncls, ng, st); else s3t_ring<kMG>(A, ncls, ng, st);
 }
-void s3_fasm(const Solve3Args& A, const Task3* t, int nt, int ncls, int ng, cudaStream_t st) {
-  if (nt) k3s_fasm<<<dim3(nt, ncls, ng), 256, 0, st>>>(A, t);
-}
-void s3_fdiag(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ng, cudaStream_t st) {
-  if (nt) k3s_fdiag<<<dim3(nbig + (nt - nbig + 7) / 8, ncls, ng), 256, 0, st>>>(A, t, nbig);
-}
-void s3_fpanel(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ng, cudaStream_t st) {
-  if (nt) k3s_fpanel<<<dim3(nbig + (nt - nbig + 7) / 8, ncls, ng), 256, 0, st>>>(A, t, nbig);
-}
-void s3_bgather(const Solve3Args& A, const Task3* t, int nt, int ncls, int ng, cudaStream_t st) {
-  if (nt) k3s_bgather<<<dim3(nt, ncls, ng), 256, 0, st>>>(A, t);
-}
-void s3_bpanel(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ng, cudaStream_t st) {
-  if (nt) k3s_bpanel<<<dim3(nbig + (nt - nbig + 7) / 8, ncls, ng), 256, 0, st>>>(A, t, nbig);
-}
-void s3_bdiag(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ng, cudaStream_t st) {
-  if (nt) k3s_bdiag<<<dim3(nbig + (nt - nbig + 7) / 8, ncls, ng), 256, 0, st>>>(A, t, nbig);
-}
+#define S3_DISPATCH(name)                                                                       \
+  void s3_##name(const Solve3Args& A, const Task3* t, int nt, int ncls, int ng, cudaStream_t st) { \
+    if (A.mg == 1) s3t_##name<1>(A, t, nt, ncls, ng, st); else s3t_##name<kMG>(A, t, nt, ncls, ng, st); \
+  }
+#define S3_DISPATCH_B(name)                                                                     \
+  void s3_##name(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ng,         \
+                 cudaStream_t st) {                                                             \
+    if (A.mg == 1) s3t_##name<1>(A, t, nt, nbig, ncls, ng, st);                                 \
+    else s3t_##name<kMG>(A, t, nt, nbig, ncls, ng, st);                                         \
+  }
+S3_DISPATCH(fasm)
+S3_DISPATCH(bgather)
+S3_DISPATCH_B(fdiag)
+S3_DISPATCH_B(fpanel)
+S3_DISPATCH_B(bpanel)
+S3_DISPATCH_B(bdiag)
 
 // ================================================================ DDM step
 // source offsets in gather order (hddm_oracle3.c kO3): 6 faces, 12 edges, 8 vertices

@@ -69,6 +69,7 @@ struct Solve3Args {
   const int* cls_mem;
   const int* flag;  // RHS t takes part iff (flag[t] != 0) == flag_on
   int flag_on;
+  int mg;           // right-hand sides per member group: 1 or kMG
 };
 constexpr int kMG = 4;  // right-hand sides per CTA pass (member group)
 
