@@ -14,6 +14,7 @@
 #include <string>
 #include <vector>
 
+#include "dense_factor.h"
 #include "engine3d.h"
 #include "kernels.cuh"
 #include "kernels3d.cuh"
@@ -473,81 +474,7 @@ void hddm3_engine::factorize() {
       aval[size_t(c) * naent + e] = cmk3(val.real(), val.imag());
     }
   }
-  cplx* d_aval = upload(aval);
-  int* d_ai = upload(Y.aent_i);
-  int* d_aj = upload(Y.aent_j);
-  int* d_ext = upload(Y.ext);
-  d_vals = dalloc<cplx>(size_t(ncls) * Y.nvals);
-  d_valsT = dalloc<cplx>(size_t(ncls) * Y.nvals);
-  CK3(cudaMemsetAsync(d_vals, 0, sizeof(cplx) * size_t(ncls) * Y.nvals, st));
-  CK3(cudaMemsetAsync(d_valsT, 0, sizeof(cplx) * size_t(ncls) * Y.nvals, st));
-  // levels by height
-  std::vector<std::vector<int>> lv(Y.max_height + 1);
-  for (int s = 0; s < nsn; ++s) lv[Y.sn[s].height].push_back(s);
-  std::vector<int*> d_lv;
-  for (auto& v : lv) d_lv.push_back(upload(v));
-  // batch of classes within the workspace budget
-  size_t freeb = 0, totb = 0;
-  CK3(cudaMemGetInfo(&freeb, &totb));
-  const double budget = std::min(0.6 * double(freeb), 64.0 * (1ull << 30));
-  const double per = double(Y.front_words) * sizeof(cplx);
-  int nb = int(std::max(1.0, std::min(double(ncls), std::floor(budget / per))));
-  if (per > budget) throw std::runtime_error("front workspace of one class exceeds device memory");
-  cplx* fronts = dalloc<cplx>(size_t(nb) * Y.front_words);
-  Fac3Args F;
-  F.sn = d_sn;
-  F.fronts = fronts;
-  F.fw = Y.front_words;
-  F.aent_i = d_ai;
-  F.aent_j = d_aj;
-  F.aval = d_aval;
-  F.naent = naent;
-  F.ext = d_ext;
-  F.vals = d_vals;
-  F.valsT = d_valsT;
-  F.nvals = Y.nvals;
-  for (int c0 = 0; c0 < ncls; c0 += nb) {
-    const int nbc = std::min(nb, ncls - c0);
-    F.cls0 = c0;
-    CK3(cudaMemsetAsync(fronts, 0, sizeof(cplx) * size_t(nbc) * Y.front_words, st));
-    for (int h = 0; h <= Y.max_height; ++h) {
-      const int nl = int(lv[h].size());
-      if (!nl) continue;
-      int maxn = 0, maxcr = 0;
-      long long maxent = 0;
-      for (int s : lv[h]) {
-        const Sn3& a = Y.sn[s];
-        maxn = std::max(maxn, a.n);
-        for (int k = 0; k < a.nch; ++k) maxcr = std::max(maxcr, int(Y.sn[a.ch[k]].rows.size()));
-        maxent = std::max(maxent, (long long)a.n * a.n + (long long)a.rows.size() * a.n);
-      }
-      f3_scatter(F, d_lv[h], nl, nbc, st);
-      f3_extadd(F, d_lv[h], nl, nbc, 0, maxcr, st);
-      f3_extadd(F, d_lv[h], nl, nbc, 1, maxcr, st);
-      for (int k0 = 0; k0 < maxn; k0 += kNB) {
-        int maxrows = 0;
-        long long maxtiles = 0;
-        for (int s : lv[h]) {
-          const Sn3& a = Y.sn[s];
-          if (a.n <= k0) continue;
-          const int b = std::min(kNB, a.n - k0), r = int(a.rows.size());
-          const int ne = std::min(a.n, k0 + b);
-          maxrows = std::max(maxrows, (a.n - k0 - b) + r + ne);
-          const long long M = a.n + r - k0 - b, T = (M + 63) / 64;
-          const long long TE = (ne + 63) / 64, TC = a.n > k0 + b ? (a.n - k0 - b + 63) / 64 : 0;
-          maxtiles = std::max(maxtiles, T * (T + 1) / 2 + TE * TC);
-        }
-        f3_dfac(F, d_lv[h], nl, nbc, k0, st);
-        f3_trsm(F, d_lv[h], nl, nbc, k0, maxrows, st);
-        f3_update(F, d_lv[h], nl, nbc, k0, maxtiles, st);
-      }
-      f3_extract(F, d_lv[h], nl, nbc, maxent, st);
-      CK3(cudaGetLastError());
-    }
-  }
-  CK3(cudaStreamSynchronize(st));
-  dfree(fronts);
-  dfree(d_aval);
+  dense_factorize(*this, Y, d_sn, ncls, aval, d_vals, d_valsT, st);
   factor_ms = now_ms3() - t0;
 }
 

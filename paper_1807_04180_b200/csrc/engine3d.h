@@ -97,4 +97,5 @@ struct Setup3 {
 
 int build_setup3(const hddm3_problem& p, Setup3& S, std::string& msg);
 
+
 }  // namespace hddm3

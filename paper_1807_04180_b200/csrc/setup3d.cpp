@@ -239,24 +239,12 @@ std::vector<int> nd_order3(int nx, int ny, int nz) {
   return S.perm;
 }
 
-void build_sym3(int nx, int ny, int nz, Sym3& S) {
-  if (nx <= 2 || ny <= 2 || nz <= 2) throw std::runtime_error("window too small for the 3-D ND solver");
-  S = Sym3();
-  S.nn[0] = nx;
-  S.nn[1] = ny;
-  S.nn[2] = nz;
-  S.n = nx * ny * nz;
-  const int n = S.n, sxy = nx * ny;
-  for (int r = 0; r < nz; ++r)
-    for (int q = 0; q < ny; ++q)
-      for (int p = 0; p < nx; ++p)
-        if (on_shell(S.nn, p, q, r)) S.perm.push_back((r * ny + q) * nx + p);
-  S.nshell = int(S.perm.size());
-  Nd3 b{nx, ny, S.perm, S.sn};
-  S.root = b.rec(1, 1, 1, nx - 2, ny - 2, nz - 2);
-  if (int(S.perm.size()) != n) throw std::runtime_error("3-D ND order is not a permutation");
-  S.pinv.assign(n, -1);
-  for (int k = 0; k < n; ++k) S.pinv[S.perm[k]] = k;
+// The dense-supernode structure of an ND tree: heights / depths, row structures, exact nnz(L), value / update /
+// front layouts, extend-add maps and the assembled-matrix scatter lists. nbr(v, k),
+// k < nk, is the k-th interior neighbour of window node v or -1.
+template <class Nbr>
+void finish_dense(Sym3& S, Nbr nbr, int nk) {
+  const int n = S.n;
   const int nsn = int(S.sn.size());
   for (int s = 0; s < nsn; ++s) {
     int hgt = 0;
@@ -270,22 +258,6 @@ void build_sym3(int nx, int ny, int nz, Sym3& S) {
       S.sn[s].depth = S.sn[S.sn[s].parent].depth + 1;
       S.max_depth = std::max(S.max_depth, S.sn[s].depth);
     }
-  // interior neighbours of a window node (-1: shell or outside)
-  auto nbr = [&](int v, int k) -> int {
-    const int p = v % nx, q = (v / nx) % ny, r = v / sxy;
-    int pp = p, qq = q, rr = r;
-    switch (k) {
-      case 0: pp = p - 1; break;
-      case 1: pp = p + 1; break;
-      case 2: qq = q - 1; break;
-      case 3: qq = q + 1; break;
-      case 4: rr = r - 1; break;
-      default: rr = r + 1; break;
-    }
-    if (pp < 0 || qq < 0 || rr < 0 || pp >= nx || qq >= ny || rr >= nz) return -1;
-    if (on_shell(S.nn, pp, qq, rr)) return -1;
-    return (rr * ny + qq) * nx + pp;
-  };
   // dense supernode row structures (postorder: children first)
   for (int s = 0; s < nsn; ++s) {
     Sn3& a = S.sn[s];
@@ -296,7 +268,7 @@ void build_sym3(int nx, int ny, int nz, Sym3& S) {
         if (r >= end) cand.push_back(r);
     for (int i = 0; i < a.n; ++i) {
       const int v = S.perm[a.c0 + i];
-      for (int k = 0; k < 6; ++k) {
+      for (int k = 0; k < nk; ++k) {
         const int u = nbr(v, k);
         if (u >= 0 && S.pinv[u] >= end) cand.push_back(S.pinv[u]);
       }
@@ -311,7 +283,7 @@ void build_sym3(int nx, int ny, int nz, Sym3& S) {
     long nnz = 0;
     for (int k = S.nshell; k < n; ++k) {
       const int v = S.perm[k];
-      for (int d = 0; d < 6; ++d) {
+      for (int d = 0; d < nk; ++d) {
         const int u = nbr(v, d);
         if (u < 0) continue;
         int i = S.pinv[u];
@@ -326,7 +298,7 @@ void build_sym3(int nx, int ny, int nz, Sym3& S) {
     for (int k = S.nshell; k < n; ++k) {
       mark[k] = k;
       const int v = S.perm[k];
-      for (int d = 0; d < 6; ++d) {
+      for (int d = 0; d < nk; ++d) {
         const int u = nbr(v, d);
         if (u < 0) continue;
         for (int i = S.pinv[u]; i >= 0 && i < k && mark[i] != k; i = parent[i]) {
@@ -425,7 +397,7 @@ void build_sym3(int nx, int ny, int nz, Sym3& S) {
       S.aent_j.push_back(j);
       S.aent_node.push_back(v);
       S.aent_kind.push_back(0);
-      for (int k = 0; k < 6; ++k) {
+      for (int k = 0; k < nk; ++k) {
         const int u = nbr(v, k);
         if (u < 0) continue;
         const int P = S.pinv[u];
@@ -446,6 +418,44 @@ void build_sym3(int nx, int ny, int nz, Sym3& S) {
     }
   }
   S.aent_ptr[nsn] = int(S.aent_i.size());
+}
+
+
+void build_sym3(int nx, int ny, int nz, Sym3& S) {
+  if (nx <= 2 || ny <= 2 || nz <= 2) throw std::runtime_error("window too small for the 3-D ND solver");
+  S = Sym3();
+  S.nn[0] = nx;
+  S.nn[1] = ny;
+  S.nn[2] = nz;
+  S.n = nx * ny * nz;
+  const int n = S.n, sxy = nx * ny;
+  for (int r = 0; r < nz; ++r)
+    for (int q = 0; q < ny; ++q)
+      for (int p = 0; p < nx; ++p)
+        if (on_shell(S.nn, p, q, r)) S.perm.push_back((r * ny + q) * nx + p);
+  S.nshell = int(S.perm.size());
+  Nd3 b{nx, ny, S.perm, S.sn};
+  S.root = b.rec(1, 1, 1, nx - 2, ny - 2, nz - 2);
+  if (int(S.perm.size()) != n) throw std::runtime_error("3-D ND order is not a permutation");
+  S.pinv.assign(n, -1);
+  for (int k = 0; k < n; ++k) S.pinv[S.perm[k]] = k;
+  // interior neighbours of a window node (-1: shell or outside)
+  auto nbr = [&](int v, int k) -> int {
+    const int p = v % nx, q = (v / nx) % ny, r = v / sxy;
+    int pp = p, qq = q, rr = r;
+    switch (k) {
+      case 0: pp = p - 1; break;
+      case 1: pp = p + 1; break;
+      case 2: qq = q - 1; break;
+      case 3: qq = q + 1; break;
+      case 4: rr = r - 1; break;
+      default: rr = r + 1; break;
+    }
+    if (pp < 0 || qq < 0 || rr < 0 || pp >= nx || qq >= ny || rr >= nz) return -1;
+    if (on_shell(S.nn, pp, qq, rr)) return -1;
+    return (rr * ny + qq) * nx + pp;
+  };
+  finish_dense(S, nbr, 6);
 }
 
 }  // namespace hddm3
