@@ -136,6 +136,21 @@ int hddm_fgmres(hddm_engine* e, const double* b, double* x, double tol,
                 hddm_fgmres_result* res, double* hist, int hist_cap,
                 hddm_stats* pstats);
 
+/* ---- sharded runs (not part of the reference surface) ----
+ * One engine per rank solves its block of subdomains: hddm_set_owned marks them
+ * (NULL: all). precondition(r, K) then runs as begin, K x (hddm_step, halo exchange),
+ * end: after step s each rank packs the solution and zero flag of its subdomains a
+ * neighbouring rank's transfers read (window-local factor order, n_w complex each),
+ * sends them, and unpacks what it receives; end returns this rank's assembled field,
+ * which the ranks sum (ddm.cpp:280-287 distributed; paper_1807_04180_b200/shard.py). */
+int hddm_set_owned(hddm_engine* e, const int* owned);
+int hddm_precondition_begin(hddm_engine* e, const double* r, int memkind);
+int hddm_step(hddm_engine* e, int s);
+int hddm_halo_pack(hddm_engine* e, int s, const int* ts, int nts, double* buf, int* flags);
+int hddm_halo_unpack(hddm_engine* e, int s, const int* ts, int nts, const double* buf,
+                     const int* flags);
+int hddm_precondition_end(hddm_engine* e, double* z, int memkind, hddm_stats* stats);
+
 /* ---- parity / measurement taps (not part of the reference surface) ---- */
 
 /* Z_j = M(V_j) of the last FGMRES restart cycle of hddm_fgmres (j < the cycle's

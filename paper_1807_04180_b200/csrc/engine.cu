@@ -118,6 +118,7 @@ struct hddm_engine {
   cplx* d_Y = nullptr;
   int* d_Z[3] = {};
   int* d_fany = nullptr;
+  int* d_owned = nullptr;  // subdomains this engine solves (sharded runs; all by default)
   int* d_cls_ptr = nullptr;
   int* d_cls_mem = nullptr;
   int* d_act_ptr = nullptr;
@@ -510,6 +511,7 @@ void hddm_engine::create(const hddm_problem& p) {
   d_Y = dalloc<cplx>(size_t(nsub) * nw);
   CK(cudaMemsetAsync(d_B, 0, size_t(nsub) * nw * sizeof(cplx), st));
   d_fany = dalloc<int>(nsub);
+  d_owned = upload(std::vector<int>(nsub, 1));
   d_zero = dalloc<int>(nsub);
   CK(cudaMemsetAsync(d_zero, 0, sizeof(int) * nsub, st));
   d_act_ptr = dalloc<int>(ncls + 1);
@@ -1179,6 +1181,7 @@ StepArgs hddm_engine::step_args(int s, const cplx* f) {
   A.act_ptr = d_act_ptr;
   A.act_list = d_act_list;
   A.counts = d_counts;
+  A.owned = d_owned;
   return A;
 }
 
@@ -1913,6 +1916,80 @@ int hddm_fgmres(hddm_engine* e, const double* b, double* x, double tol, int max_
       pstats->skipped += long(cnt[1]);
       pstats->sweep_ms += sweep_ms;
       pstats->factor_ms = e->factor_ms;
+    }
+  });
+}
+
+// ---- sharded runs: one engine per rank, each solving its block of
+// subdomains; the ranks exchange the solutions and zero flags of the subdomains at
+// their block boundaries after every step and sum their assembled fields at the end
+// (paper_1807_04180_b200/shard.py drives it over torch.distributed).
+int hddm_set_owned(hddm_engine* e, const int* owned) {
+  return guarded(e, [&] {
+    std::vector<int> o(e->nsub, 1);
+    if (owned)
+      for (int t = 0; t < e->nsub; ++t) o[t] = owned[t] ? 1 : 0;
+    CK(cudaMemcpyAsync(e->d_owned, o.data(), sizeof(int) * e->nsub, cudaMemcpyHostToDevice, e->st));
+    CK(cudaStreamSynchronize(e->st));
+  });
+}
+
+int hddm_precondition_begin(hddm_engine* e, const double* r, int memkind) {
+  return guarded(e, [&] {
+    const cplx* dr = in_ptr(e, r, memkind, e->d_f);
+    if (dr != e->d_f)
+      CK(cudaMemcpyAsync(e->d_f, dr, e->ng * sizeof(cplx), cudaMemcpyDeviceToDevice, e->st));
+    e->reset_state();
+    CK(cudaMemsetAsync(e->d_counts, 0, 2 * sizeof(long long), e->st));
+    CK(cudaMemsetAsync(e->d_refine, 0, sizeof(int), e->st));
+    CK(cudaMemsetAsync(e->d_maxrel, 0, sizeof(double), e->st));
+    launch_fany(e->step_args(1, e->d_f), e->st);
+  });
+}
+
+int hddm_step(hddm_engine* e, int s) {
+  return guarded(e, [&] {
+    if (s < 1 || s != e->last_step + 1) throw ConfigErr("steps run in order from 1 after hddm_precondition_begin");
+    e->run_step(s);
+  });
+}
+
+int hddm_halo_pack(hddm_engine* e, int s, const int* ts, int nts, double* buf, int* flags) {
+  return guarded(e, [&] {
+    if (s < 1 || s != e->last_step) throw ConfigErr("halo of a step that has not run");
+    cplx* b = reinterpret_cast<cplx*>(buf);
+    for (int k = 0; k < nts; ++k) {
+      if (ts[k] < 0 || ts[k] >= e->nsub) throw ConfigErr("no such subdomain");
+      e->get_vec(e->d_U[s % 3], ts[k], b + size_t(k) * e->nw, e->st);
+      CK(cudaMemcpyAsync(flags + k, e->d_Z[s % 3] + ts[k], sizeof(int), cudaMemcpyDeviceToHost, e->st));
+    }
+    CK(cudaStreamSynchronize(e->st));
+  });
+}
+
+int hddm_halo_unpack(hddm_engine* e, int s, const int* ts, int nts, const double* buf, const int* flags) {
+  return guarded(e, [&] {
+    if (s < 1 || s != e->last_step) throw ConfigErr("halo of a step that has not run");
+    const cplx* b = reinterpret_cast<const cplx*>(buf);
+    for (int k = 0; k < nts; ++k) {
+      if (ts[k] < 0 || ts[k] >= e->nsub) throw ConfigErr("no such subdomain");
+      e->put_vec(e->d_U[s % 3], ts[k], b + size_t(k) * e->nw, e->st);
+      CK(cudaMemcpyAsync(e->d_Z[s % 3] + ts[k], flags + k, sizeof(int), cudaMemcpyHostToDevice, e->st));
+    }
+    CK(cudaStreamSynchronize(e->st));
+  });
+}
+
+int hddm_precondition_end(hddm_engine* e, double* z, int memkind, hddm_stats* stats) {
+  return guarded(e, [&] {
+    out_copy(e, z, e->d_asm, memkind);
+    long long cnt[2];
+    read_counts(e, cnt);
+    check_refine(e);
+    if (stats) {
+      stats->solves += long(cnt[0]);
+      stats->skipped += long(cnt[1]);
+      stats->factor_ms = e->factor_ms;
     }
   });
 }

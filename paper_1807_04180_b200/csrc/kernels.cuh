@@ -183,6 +183,9 @@ struct StepArgs {
   int* act_ptr;
   int* act_list;
   long long* counts;     // [0] solves, [1] skipped
+  const int* owned;      // sharded runs (hddm_set_owned): subdomains this engine solves;
+                         // the others are skipped here, their flags / solutions set by
+                         // hddm_halo_unpack; null: every subdomain
 };
 
 void launch_fany(const StepArgs& A, cudaStream_t st);

@@ -59,7 +59,15 @@ void launch_fany(const StepArgs& A, cudaStream_t st) {
 // zero flags, active lists per class, solve/skip counters (ddm.cpp:187-207)
 __global__ void k_flags(StepArgs A, int ncls) {
   extern __shared__ int sh[];  // ncls counts
+  __shared__ int nown;
+  if (threadIdx.x == 0) nown = 0;
+  __syncthreads();
   for (int t = threadIdx.x; t < A.nsub; t += blockDim.x) {
+    if (A.owned && !A.owned[t]) {  // another engine's subdomain (sharded run)
+      A.zc[t] = 1;
+      continue;
+    }
+    atomicAdd(&nown, 1);
     const DevSub S = A.sub[t];
     int any = (A.step == 1) ? A.fany[t] : 0;
     for (int d = 0; d < 8; ++d) {
@@ -85,7 +93,7 @@ __global__ void k_flags(StepArgs A, int ncls) {
     }
     A.act_ptr[ncls] = acc;
     A.counts[0] += acc;
-    A.counts[1] += A.nsub - acc;
+    A.counts[1] += nown - acc;
   }
   __syncthreads();
   for (int c = threadIdx.x; c < ncls; c += blockDim.x) {

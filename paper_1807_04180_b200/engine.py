@@ -156,6 +156,12 @@ def load_library(path: str = LIB_PATH):
         "hddm_time_kernel": (C.c_int, [vp, C.c_int, C.c_int, dp]),
         "hddm_stage_name": (C.c_char_p, [C.c_int]),
         "hddm_stream": (vp, [vp]),
+        "hddm_set_owned": (C.c_int, [vp, ip]),
+        "hddm_precondition_begin": (C.c_int, [vp, vp, C.c_int]),
+        "hddm_step": (C.c_int, [vp, C.c_int]),
+        "hddm_halo_pack": (C.c_int, [vp, C.c_int, ip, C.c_int, dp, ip]),
+        "hddm_halo_unpack": (C.c_int, [vp, C.c_int, ip, C.c_int, dp, ip]),
+        "hddm_precondition_end": (C.c_int, [vp, vp, C.c_int, P(_Stats)]),
         "hddm_solver_desc": (C.c_char_p, [vp]),
     }
     for name, (res, args) in sigs.items():
@@ -468,3 +474,53 @@ class DdmEngine:
 
     def stream_handle(self) -> int:
         return int(self.lib.hddm_stream(self.h) or 0)
+
+    # -- sharded runs (hddm.h "sharded runs"; driven by shard.py)
+    def set_owned(self, owned):
+        """Subdomains this engine solves (None: all)."""
+        if owned is None:
+            self._check(self.lib.hddm_set_owned(self.h, None))
+            return
+        o = np.ascontiguousarray(owned, np.int32)
+        self._check(self.lib.hddm_set_owned(self.h, o.ctypes.data_as(C.POINTER(C.c_int))))
+
+    def precondition_begin(self, r):
+        pr, mk, keep = self._io(r)
+        self._check(self.lib.hddm_precondition_begin(self.h, pr, mk))
+        self._begin_kind = mk
+
+    def step(self, s: int):
+        self._check(self.lib.hddm_step(self.h, s))
+
+    def halo_pack(self, s: int, ts):
+        """(solutions [len(ts), n_w] complex, zero flags) of subdomains ts after step s."""
+        ts = np.ascontiguousarray(ts, np.int32)
+        nw = int(np.prod(self.window_dims()))
+        buf = np.empty((len(ts), nw), np.complex128)
+        flags = np.empty(len(ts), np.int32)
+        ip = C.POINTER(C.c_int)
+        self._check(self.lib.hddm_halo_pack(self.h, s, ts.ctypes.data_as(ip), len(ts),
+                                            buf.ctypes.data_as(C.POINTER(C.c_double)),
+                                            flags.ctypes.data_as(ip)))
+        return buf, flags
+
+    def halo_unpack(self, s: int, ts, buf, flags):
+        ts = np.ascontiguousarray(ts, np.int32)
+        buf = np.ascontiguousarray(buf, np.complex128)
+        flags = np.ascontiguousarray(flags, np.int32)
+        ip = C.POINTER(C.c_int)
+        self._check(self.lib.hddm_halo_unpack(self.h, s, ts.ctypes.data_as(ip), len(ts),
+                                              buf.ctypes.data_as(C.POINTER(C.c_double)),
+                                              flags.ctypes.data_as(ip)))
+
+    def precondition_end(self, stats: Optional[DdmStats] = None):
+        """This engine's assembled field (numpy, host) after the sharded sweeps."""
+        z = np.empty(self.n, np.complex128)
+        st = _Stats()
+        self._check(self.lib.hddm_precondition_end(self.h, C.c_void_p(z.ctypes.data), HDDM_HOST,
+                                                   C.byref(st)))
+        if stats is not None:
+            stats.solves += st.solves
+            stats.skipped += st.skipped
+        return z
+
