@@ -150,6 +150,14 @@ int hddm_halo_pack(hddm_engine* e, int s, const int* ts, int nts, double* buf, i
 int hddm_halo_unpack(hddm_engine* e, int s, const int* ts, int nts, const double* buf,
                      const int* flags);
 int hddm_precondition_end(hddm_engine* e, double* z, int memkind, hddm_stats* stats);
+/* FGMRES over the sharded preconditioner: with a hook set, hddm_fgmres runs its restart
+ * cycles host-driven and calls fn(user, 1, s) after every DDM step s (the caller
+ * exchanges halos there) and fn(user, 2, K) after the K steps of each preconditioner
+ * application (the caller sums the ranks' assembled fields, hddm_assembled read /
+ * write = 0 / 1). Every rank runs the same Krylov recurrence on identical vectors. */
+typedef void (*hddm_step_hook)(void* user, int stage, int s);
+int hddm_set_step_hook(hddm_engine* e, hddm_step_hook fn, void* user);
+int hddm_assembled(hddm_engine* e, double* buf, int write);
 
 /* ---- parity / measurement taps (not part of the reference surface) ---- */
 

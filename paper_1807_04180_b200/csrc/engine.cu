@@ -119,6 +119,10 @@ struct hddm_engine {
   int* d_Z[3] = {};
   int* d_fany = nullptr;
   int* d_owned = nullptr;  // subdomains this engine solves (sharded runs; all by default)
+  // sharded runs: called after every DDM step (stage 1, s) and after the K steps of a
+  // preconditioner application (stage 2, K) of the host-driven Krylov cycle
+  hddm_step_hook hook = nullptr;
+  void* hook_user = nullptr;
   int* d_cls_ptr = nullptr;
   int* d_cls_mem = nullptr;
   int* d_act_ptr = nullptr;
@@ -1517,11 +1521,14 @@ int hddm_engine::enqueue_kry_iteration(int K, unsigned long long cond, cudaGraph
   launch_fany(step_args(1, d_f), st);
   nk += 2;
   for (int s = 1; s <= K; ++s) {
-    if (body)
+    if (body) {
       nk += capture_step(s, body);
-    else
+    } else {
       run_step(s);
+      if (hook) hook(hook_user, 1, s);  // halo exchange of a sharded run
+    }
   }
+  if (!body && hook) hook(hook_user, 2, K);  // sum of the ranks' assembled fields
   launch_kry_store(KA, d_asm, st);
   GlobalArgs G{S.gnx, S.gny, 1.0 / (S.h * S.h), d_ga, d_k2};
   launch_apply_global_ind(G, d_Zptr, 0, d_Vptr, 1, &d_ks->j, st);
@@ -1565,7 +1572,7 @@ void hddm_engine::build_kry_graph(int K) {
 void hddm_engine::launch_kry_cycle(int K, int m) {
   (void)m;
   static const bool no_graphs = std::getenv("HDDM_NO_GRAPHS") != nullptr;
-  if (no_graphs) {  // host-driven (profiling): one sync per iteration
+  if (no_graphs || hook) {  // host-driven (profiling, sharded runs): one sync per iteration
     for (;;) {
       enqueue_kry_iteration(K, 0, nullptr);
       CK(cudaMemcpyAsync(h_ks, d_ks, sizeof(KryState), cudaMemcpyDeviceToHost, st));
@@ -1976,6 +1983,22 @@ int hddm_halo_unpack(hddm_engine* e, int s, const int* ts, int nts, const double
       e->put_vec(e->d_U[s % 3], ts[k], b + size_t(k) * e->nw, e->st);
       CK(cudaMemcpyAsync(e->d_Z[s % 3] + ts[k], flags + k, sizeof(int), cudaMemcpyHostToDevice, e->st));
     }
+    CK(cudaStreamSynchronize(e->st));
+  });
+}
+
+int hddm_set_step_hook(hddm_engine* e, hddm_step_hook fn, void* user) {
+  return guarded(e, [&] {
+    e->hook = fn;
+    e->hook_user = user;
+  });
+}
+
+int hddm_assembled(hddm_engine* e, double* buf, int write) {
+  return guarded(e, [&] {
+    CK(cudaMemcpyAsync(write ? static_cast<void*>(e->d_asm) : static_cast<void*>(buf),
+                       write ? static_cast<const void*>(buf) : static_cast<const void*>(e->d_asm),
+                       e->ng * sizeof(cplx), write ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, e->st));
     CK(cudaStreamSynchronize(e->st));
   });
 }

@@ -108,6 +108,7 @@ class FgmresResult:
 
 
 _lib = None
+HOOK = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.c_int)  # hddm_step_hook
 _OPTIONAL = {"hddm_fgmres_z", "hddm_solver_desc"}
 
 
@@ -162,6 +163,8 @@ def load_library(path: str = LIB_PATH):
         "hddm_halo_pack": (C.c_int, [vp, C.c_int, ip, C.c_int, dp, ip]),
         "hddm_halo_unpack": (C.c_int, [vp, C.c_int, ip, C.c_int, dp, ip]),
         "hddm_precondition_end": (C.c_int, [vp, vp, C.c_int, P(_Stats)]),
+        "hddm_set_step_hook": (C.c_int, [vp, HOOK, vp]),
+        "hddm_assembled": (C.c_int, [vp, dp, C.c_int]),
         "hddm_solver_desc": (C.c_char_p, [vp]),
     }
     for name, (res, args) in sigs.items():
@@ -523,4 +526,20 @@ class DdmEngine:
             stats.solves += st.solves
             stats.skipped += st.skipped
         return z
+
+    def set_step_hook(self, fn):
+        """fn(stage, s) after every DDM step (stage 1) and every preconditioner
+        application (stage 2) of a host-driven FGMRES (sharded runs); None clears it."""
+        self._hook = HOOK(lambda user, stage, s: fn(stage, s)) if fn else C.cast(None, HOOK)
+        self._check(self.lib.hddm_set_step_hook(self.h, self._hook, None))
+
+    def assembled(self, values=None):
+        """Read (values None) or write the engine's assembled field (host numpy)."""
+        dp = C.POINTER(C.c_double)
+        if values is None:
+            a = np.empty(self.n, np.complex128)
+            self._check(self.lib.hddm_assembled(self.h, a.ctypes.data_as(dp), 0))
+            return a
+        a = np.ascontiguousarray(values, np.complex128)
+        self._check(self.lib.hddm_assembled(self.h, a.ctypes.data_as(dp), 1))
 

@@ -158,3 +158,37 @@ class ShardedDdm:
             stats.solves += int(cnt[0])
             stats.skipped += int(cnt[1])
         return zt.numpy().view(np.complex128)
+
+    def fgmres(self, b, opt, ksteps: int, pstats=None):
+        """fgmres(A = apply_global, M = the sharded precondition(K)) as cli.cpp:210-228
+        wires it: every rank runs the engine's device FGMRES on identical vectors; its
+        host-driven cycles call back after every step (halo exchange) and after every
+        preconditioner application (all_reduce of the assembled fields). Returns
+        (x, FgmresResult) on every rank; pstats accumulates solves / skips of all ranks."""
+        import torch
+        from .engine import DdmStats
+        e = self.eng
+
+        def hook(stage, s):
+            if stage == 1:
+                self._tag += 1
+                exchange(self.plan, lambda ts: e.halo_pack(s, ts),
+                         lambda ts, bb, f: e.halo_unpack(s, ts, bb, f), self._tag, self.nw, self.dist)
+            else:
+                a = torch.from_numpy(e.assembled().view(np.float64).copy())
+                self.dist.all_reduce(a)
+                e.assembled(a.numpy().view(np.complex128))
+
+        st = DdmStats()
+        e.set_step_hook(hook)
+        try:
+            x, res = e.fgmres(b, opt, ksteps, st)
+        finally:
+            e.set_step_hook(None)
+        cnt = torch.tensor([st.solves, st.skipped], dtype=torch.int64)
+        self.dist.all_reduce(cnt)
+        if pstats is not None:
+            pstats.solves += int(cnt[0])
+            pstats.skipped += int(cnt[1])
+        return x, res
+

@@ -49,10 +49,14 @@ def _rank(rank, world, port, name, out):
         st = DdmStats()
         z = sh.precondition(f, k, st)
         res[k] = (z, st.solves, st.skipped)
+    from paper_1807_04180_b200.engine import FgmresOptions
+    ps = DdmStats()
+    x, fr = sh.fgmres(f, FgmresOptions(1e-8, 40, 30), K, ps)
     sh.close()
     if rank == 0:
         out["res"] = {k: (v[0].tobytes(), v[1], v[2]) for k, v in res.items()}
         out["mine"] = len(sh.plan.mine)
+        out["fg"] = (x.tobytes(), fr.iters, fr.converged, list(fr.history), ps.solves, ps.skipped)
     dist.destroy_process_group()
 
 
@@ -64,6 +68,7 @@ def test_sharded_precondition_matches_single_engine(name):
     mp.spawn(_rank, args=(2, _free_port(), name, out), nprocs=2, join=True)
     prob, K = _case(name)
     f = prob.source_f()
+    from paper_1807_04180_b200.engine import FgmresOptions
     with DdmEngine(prob) as e:
         for k, (zb, solves, skipped) in out["res"].items():
             st = DdmStats()
@@ -71,4 +76,13 @@ def test_sharded_precondition_matches_single_engine(name):
             z = np.frombuffer(zb, np.complex128)
             assert np.linalg.norm(z - z1) <= 1e-12 * np.linalg.norm(z1), k
             assert (solves, skipped) == (st.solves, st.skipped), k
+        # FGMRES(30) over the sharded preconditioner: same iterations, x, history, counts
+        ps = DdmStats()
+        x1, r1 = e.fgmres(f, FgmresOptions(1e-8, 40, 30), K, ps)
+        xb, iters, conv, hist, solves, skipped = out["fg"]
+        x = np.frombuffer(xb, np.complex128)
+        assert (iters, conv) == (r1.iters, r1.converged)
+        assert np.linalg.norm(x - x1) <= 1e-10 * np.linalg.norm(x1)
+        np.testing.assert_allclose(hist, r1.history, rtol=1e-6, atol=1e-13)
+        assert (solves, skipped) == (ps.solves, ps.skipped)
     assert out["mine"] == prob.n1 * prob.n2 // 2
