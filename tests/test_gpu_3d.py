@@ -250,3 +250,24 @@ def test_config5_local_solves(cfg5):
     for c in (0, 7):
         x, rel = e.class_solve(c, b)
         assert rel <= 1e-11 and np.isfinite(x).all()
+
+
+def test_config5_sweeps_match_restatement_fingerprint(cfg5):
+    """precondition(f, K = 1, 2) at full size against the 3-D restatement's own run
+    (tests/golden/make_golden_cfg5.py; its factorization took 35 min, so the vectors
+    travel as 4096 seeded samples, 16 seeded projections and the norm)."""
+    import os
+    import sys
+    from conftest import GOLDEN
+    sys.path.insert(0, GOLDEN)
+    from make_golden_cfg5 import fingerprint, fingerprint_basis
+    prob, e = cfg5
+    g = np.load(os.path.join(GOLDEN, "cfg5_fingerprint.npz"))
+    idx, W = fingerprint_basis(prob.n_global)
+    assert np.array_equal(idx, g["idx"])
+    f = prob.source_f()
+    for k in (1, 2):
+        s, p, nrm = fingerprint(e.precondition(f, k), idx, W)
+        assert rel_l2(s, g[f"z{k}_samples"]) <= 1e-10, k
+        assert rel_l2(p, g[f"z{k}_proj"]) <= 1e-10, k
+        assert abs(nrm - float(g[f"z{k}_norm"])) <= 1e-10 * float(g[f"z{k}_norm"]), k
