@@ -89,6 +89,11 @@ struct hddm3_engine {
   int cop_stride = 0;
   double* d_wts = nullptr;
   int* d_cov = nullptr;
+  // transfer tables (k3d_rhs_xfer)
+  int npatch = 0;
+  int *d_pnode = nullptr, *d_pent = nullptr, *d_edir = nullptr, *d_esrc = nullptr;
+  double* d_ebeta = nullptr;
+  void build_transfer_tables();
   cplx* d_U[4] = {};
   int* d_Z[4] = {};
   cplx *d_B = nullptr, *d_Y = nullptr, *d_UPD = nullptr, *d_R = nullptr, *d_C = nullptr;
@@ -308,6 +313,7 @@ void hddm3_engine::create(const hddm3_problem& p) {
       }
     d_cov = upload(cov);
   }
+  build_transfer_tables();
   for (int k = 0; k < 4; ++k) {
     d_U[k] = dalloc<cplx>(size_t(nsub) * nw);
     d_Z[k] = dalloc<int>(nsub);
@@ -351,6 +357,82 @@ void hddm3_engine::create(const hddm3_problem& p) {
   d_scal = dalloc<double>(64);
   factorize();
   run_probe();
+}
+
+// Structural transfer tables (transfer_patch / transfer_beta in 3-D, hddm_oracle3.c):
+// every window has the same shape and its core at the same local offset, so the union of
+// the 26 patches, the directions covering each of its nodes, the source-window position
+// of each of the 7 stencil points and their tapers are window-local and computed once.
+// Nodes in factor order (coalesced writes of b); entries per node in gather order.
+void hddm3_engine::build_transfer_tables() {
+  static const int kO[26][3] = {
+      {+1, 0, 0}, {-1, 0, 0}, {0, +1, 0}, {0, -1, 0}, {0, 0, +1}, {0, 0, -1},
+      {+1, +1, 0}, {-1, +1, 0}, {+1, -1, 0}, {-1, -1, 0},
+      {+1, 0, +1}, {-1, 0, +1}, {+1, 0, -1}, {-1, 0, -1},
+      {0, +1, +1}, {0, -1, +1}, {0, +1, -1}, {0, -1, -1},
+      {+1, +1, +1}, {-1, +1, +1}, {+1, -1, +1}, {-1, -1, +1},
+      {+1, +1, -1}, {-1, +1, -1}, {+1, -1, -1}, {-1, -1, -1}};
+  static const int kDp[7][3] = {{0, 0, 0}, {1, 0, 0}, {-1, 0, 0}, {0, 1, 0}, {0, -1, 0}, {0, 0, 1}, {0, 0, -1}};
+  const int* nn = Y.nn;
+  const int nov = S.nov, c0L = S.ext;  // window-local core: [ext, ext + mc] per axis
+  auto beta0h = [](double t) {
+    if (t <= 0) return 1.0;
+    if (t >= 1) return 0.0;
+    return 1.0 - t * t * t * (10.0 - 15.0 * t + 6.0 * t * t);
+  };
+  std::vector<int> pnode, pent(1, 0), edir, esrc;
+  std::vector<double> ebeta;
+  for (int pos = 0; pos < nw; ++pos) {
+    const int v = Y.perm[pos];
+    const int L[3] = {v % nn[0], (v / nn[0]) % nn[1], v / (nn[0] * nn[1])};
+    bool interior = true;
+    for (int a = 0; a < 3; ++a) interior = interior && L[a] > 0 && L[a] < nn[a] - 1;
+    if (!interior) continue;
+    int cnt = 0;
+    for (int d = 0; d < 26; ++d) {
+      bool in = true;
+      for (int a = 0; a < 3; ++a) {
+        const int o = kO[d][a], e1 = S.ext + S.mc[a];  // window-local core [ext, ext + mc]
+        if (o > 0) in = in && L[a] >= e1 - 1 - nov && L[a] <= e1 - 1;
+        if (o < 0) in = in && L[a] >= c0L + 1 && L[a] <= c0L + 1 + nov;
+      }
+      if (!in) continue;
+      ++cnt;
+      edir.push_back(d);
+      for (int k = 0; k < 7; ++k) {
+        int ls[3], G[3];
+        bool inside = true;
+        for (int a = 0; a < 3; ++a) {
+          G[a] = L[a] + kDp[k][a];                 // target-local (= global - w0_t)
+          ls[a] = G[a] - kO[d][a] * S.mc[a];       // source-local
+          inside = inside && ls[a] >= 0 && ls[a] < nn[a];
+        }
+        esrc.push_back(inside ? Y.pinv[(ls[2] * nn[1] + ls[1]) * nn[0] + ls[0]] : -1);
+        double b = 1.0;
+        bool first = true;
+        for (int a = 0; a < 3; ++a) {
+          const int o = kO[d][a], e1 = S.ext + S.mc[a];
+          if (!o) continue;
+          const double bv = o > 0 ? beta0h(double(e1 - 1 - G[a]) / nov) : beta0h(double(G[a] - c0L - 1) / nov);
+          b = first ? bv : b * bv;
+          first = false;
+        }
+        ebeta.push_back(b);
+      }
+    }
+    if (cnt) {
+      pnode.push_back(v);
+      pent.push_back(int(edir.size()));
+    }
+  }
+  npatch = int(pnode.size());
+  if (npatch) {
+    d_pnode = upload(pnode);
+    d_pent = upload(pent);
+    d_edir = upload(edir);
+    d_esrc = upload(esrc);
+    d_ebeta = upload(ebeta);
+  }
 }
 
 // Task lists: forward levels by height (leaves first), backward levels by depth.
@@ -637,6 +719,12 @@ Step3Args hddm3_engine::step_args(int s, const cplx* f) {
   A.cov = d_cov;
   A.step = s;
   A.counts = d_counts;
+  A.npatch = npatch;
+  A.pnode = d_pnode;
+  A.pent = d_pent;
+  A.edir = d_edir;
+  A.esrc = d_esrc;
+  A.ebeta = d_ebeta;
   return A;
 }
 

@@ -810,93 +810,88 @@ __device__ __forceinline__ cplx jac3(const CoefP& K, int p, int q, int r) {
 }
 }  // namespace
 
-// right-hand sides (sweep, ddm.cpp:174-205 in 3-D): b = J (f on the owned box at
-// step 1 - the 26 tapered transfers L_t(beta_d v_src)), thread per (node, t)
-__global__ void __launch_bounds__(128) k3d_rhs(Step3Args A) {
+// right-hand sides (sweep, ddm.cpp:174-205 in 3-D), two passes: (1) every window
+// node of an active subdomain: b = J f on the owned box at step 1, else 0 (shell 0);
+// (2) the nodes of the union of the 26 transfer patches (structural tables built on the
+// host): b = J (f_owned - sum_d L_t(beta_d v_src)) over the directions in gather order
+// whose source exists and is not zero-flagged, the source values and tapers of the 7
+// stencil points read from the tables. Thread per (node, t).
+__global__ void __launch_bounds__(256) k3d_rhs_base(Step3Args A) {
   const int t = blockIdx.y;
   if (A.zc[t]) return;
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= A.nw) return;
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= A.nw) return;
+  const int v = A.perm[pos];
   const int nx = A.nn[0], ny = A.nn[1];
   const int p = v % nx, q = (v / nx) % ny, r = v / (nx * ny);
-  const long long o = (long long)t * A.nw + A.pinv[v];
-  if (shell3(A.nn, p, q, r)) {
-    A.B[o] = cmk(0, 0);
-    return;
+  cplx b = cmk(0, 0);
+  if (A.step == 1 && !shell3(A.nn, p, q, r)) {
+    const Sub3Dev s = A.sub[t];
+    const int P[3] = {s.w0[0] + p, s.w0[1] + q, s.w0[2] + r};
+    bool own = true;
+    for (int a = 0; a < 3; ++a) own = own && P[a] >= s.own0[a] && P[a] <= s.own1[a];
+    if (own) {
+      const CoefP K = coefs(A.cop, A.cop_stride, s.cls, A.nn);
+      b = cmul(jac3(K, p, q, r), A.f[((long long)P[2] * A.gn[1] + P[1]) * A.gn[0] + P[0]]);
+    }
   }
+  A.B[(long long)t * A.nw + pos] = b;
+}
+
+__global__ void __launch_bounds__(128) k3d_rhs_xfer(Step3Args A) {
+  const int t = blockIdx.y;
+  if (A.zc[t]) return;
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= A.npatch) return;
+  const int v = A.pnode[u];
+  const int nx = A.nn[0], ny = A.nn[1];
+  const int p = v % nx, q = (v / nx) % ny, r = v / (nx * ny);
   const Sub3Dev s = A.sub[t];
-  const int P[3] = {s.w0[0] + p, s.w0[1] + q, s.w0[2] + r};
-  const int L[3] = {p, q, r};
   cplx acc = cmk(0, 0);
   if (A.step == 1) {
+    const int P[3] = {s.w0[0] + p, s.w0[1] + q, s.w0[2] + r};
     bool own = true;
     for (int a = 0; a < 3; ++a) own = own && P[a] >= s.own0[a] && P[a] <= s.own1[a];
     if (own) acc = A.f[((long long)P[2] * A.gn[1] + P[1]) * A.gn[0] + P[0]];
   }
   const CoefP K = coefs(A.cop, A.cop_stride, s.cls, A.nn);
-  for (int d = 0; d < 26; ++d) {
+  const cplx ex = cscale(cmul(K.an[1][q], K.an[2][r]), A.ih2);
+  const cplx ey = cscale(cmul(K.an[0][p], K.an[2][r]), A.ih2);
+  const cplx ez = cscale(cmul(K.an[0][p], K.an[1][q]), A.ih2);
+  const cplx jac = jac3(K, p, q, r);
+  for (int e = A.pent[u]; e < A.pent[u + 1]; ++e) {
+    const int d = A.edir[e];
     int si[3];
     bool ok = true;
     for (int a = 0; a < 3; ++a) {
-      const int o3 = kO3[d][a];
-      si[a] = s.ix[a] + o3;
+      si[a] = s.ix[a] + kO3[d][a];
       ok = ok && si[a] >= 0 && si[a] < A.n[a];
-      // patch of direction d (transfer_patch in 3-D), window-local interior range
-      if (o3 > 0) ok = ok && P[a] >= s.c1[a] - 1 - A.nov && P[a] <= s.c1[a] - 1;
-      if (o3 < 0) ok = ok && P[a] >= s.c0[a] + 1 && P[a] <= s.c0[a] + 1 + A.nov;
     }
     if (!ok) continue;
     const int lag = (kO3[d][0] != 0) + (kO3[d][1] != 0) + (kO3[d][2] != 0);
     const int src = sub_index(A, si[0], si[1], si[2]);
     if (A.zp[lag - 1][src]) continue;
-    const Sub3Dev so = A.sub[src];
     const cplx* vs = A.Up[lag - 1] + (long long)src * A.nw;
-    // w at the 7 stencil points: beta_d(point) * v_src(point), 0 outside the source window
+    const int* sp = A.esrc + 7LL * e;
+    const double* bt = A.ebeta + 7LL * e;
     cplx w[7];
-    const int dp[7][3] = {{0, 0, 0}, {1, 0, 0}, {-1, 0, 0}, {0, 1, 0}, {0, -1, 0}, {0, 0, 1}, {0, 0, -1}};
 #pragma unroll
     for (int k = 0; k < 7; ++k) {
-      int G[3], l[3];
-      bool in = true;
-      for (int a = 0; a < 3; ++a) {
-        G[a] = P[a] + dp[k][a];
-        l[a] = G[a] - so.w0[a];
-        in = in && l[a] >= 0 && l[a] < A.nn[a];
-      }
-      cplx val = cmk(0, 0);
-      if (in) {
-        const cplx x = vs[A.pinv[(l[2] * ny + l[1]) * nx + l[0]]];
-        if (x.x != 0.0 || x.y != 0.0) {
-          double b = 1.0;
-          bool first = true;
-          for (int a = 0; a < 3; ++a) {
-            const int o3 = kO3[d][a];
-            if (!o3) continue;
-            const double bv = o3 > 0 ? hddm::beta0(double(s.c1[a] - 1 - G[a]) / A.nov)
-                                     : hddm::beta0(double(G[a] - s.c0[a] - 1) / A.nov);
-            b = first ? bv : b * bv;
-            first = false;
-          }
-          val = cscale(x, b);
-        }
-      }
-      w[k] = val;
+      const int ps = sp[k];
+      const cplx x = ps >= 0 ? vs[ps] : cmk(0, 0);
+      w[k] = (x.x != 0.0 || x.y != 0.0) ? cscale(x, bt[k]) : cmk(0, 0);
     }
     // L-form 7-point stencil with the target's coefficients (hddm_oracle3.c stencil3)
-    const cplx ex = cscale(cmul(K.an[1][L[1]], K.an[2][L[2]]), A.ih2);
-    const cplx ey = cscale(cmul(K.an[0][L[0]], K.an[2][L[2]]), A.ih2);
-    const cplx ez = cscale(cmul(K.an[0][L[0]], K.an[1][L[1]]), A.ih2);
     const cplx uc = w[0];
-    cplx tt = cmul(cmul(ex, K.iah[0][L[0]]), csub(w[1], uc));
-    tt = csub(tt, cmul(cmul(ex, K.iah[0][L[0] - 1]), csub(uc, w[2])));
-    tt = cadd(tt, cmul(cmul(ey, K.iah[1][L[1]]), csub(w[3], uc)));
-    tt = csub(tt, cmul(cmul(ey, K.iah[1][L[1] - 1]), csub(uc, w[4])));
-    tt = cadd(tt, cmul(cmul(ez, K.iah[2][L[2]]), csub(w[5], uc)));
-    tt = csub(tt, cmul(cmul(ez, K.iah[2][L[2] - 1]), csub(uc, w[6])));
-    const cplx st = cadd(cdiv(tt, jac3(K, p, q, r)), cscale(uc, A.k2));
-    acc = csub(acc, st);
+    cplx tt = cmul(cmul(ex, K.iah[0][p]), csub(w[1], uc));
+    tt = csub(tt, cmul(cmul(ex, K.iah[0][p - 1]), csub(uc, w[2])));
+    tt = cadd(tt, cmul(cmul(ey, K.iah[1][q]), csub(w[3], uc)));
+    tt = csub(tt, cmul(cmul(ey, K.iah[1][q - 1]), csub(uc, w[4])));
+    tt = cadd(tt, cmul(cmul(ez, K.iah[2][r]), csub(w[5], uc)));
+    tt = csub(tt, cmul(cmul(ez, K.iah[2][r - 1]), csub(uc, w[6])));
+    acc = csub(acc, cadd(cdiv(tt, jac), cscale(uc, A.k2)));
   }
-  A.B[o] = cmul(jac3(K, p, q, r), acc);
+  A.B[(long long)t * A.nw + A.pinv[v]] = cmul(jac, acc);
 }
 
 // blend-accumulate (accumulate_weighted in 3-D): thread per global node, the
@@ -947,7 +942,8 @@ __global__ void __launch_bounds__(256) k3d_accumulate(Step3Args A, const double*
 void d3_fany(const Step3Args& A, cudaStream_t st) { k3d_fany<<<A.nsub, 256, 0, st>>>(A); }
 void d3_flags(const Step3Args& A, cudaStream_t st) { k3d_flags<<<1, 256, 0, st>>>(A); }
 void d3_rhs(const Step3Args& A, cudaStream_t st) {
-  k3d_rhs<<<dim3((A.nw + 127) / 128, A.nsub), 128, 0, st>>>(A);
+  k3d_rhs_base<<<dim3((A.nw + 255) / 256, A.nsub), 256, 0, st>>>(A);
+  if (A.npatch) k3d_rhs_xfer<<<dim3((A.npatch + 127) / 128, A.nsub), 128, 0, st>>>(A);
 }
 void d3_accumulate(const Step3Args& A, cudaStream_t st) {
   k3d_accumulate<<<hddm::reduce_blocks(), 256, 0, st>>>(A, A.wts);

@@ -112,11 +112,19 @@ struct Step3Args {
   const int* cov;    // per axis a, global coordinate P: two covering subdomain indices (or -1)
   int step;
   long long* counts; // solves, skipped
+  // transfer tables (window-local, identical for every window): the nodes of the union
+  // of the 26 patches, per node its (direction, 7 source positions, 7 tapers) entries
+  int npatch;
+  const int* pnode;      // window node
+  const int* pent;       // npatch + 1: entry range per node
+  const int* edir;       // per entry: direction (gather order)
+  const int* esrc;       // per entry: 7 source-window factor positions (-1: outside)
+  const double* ebeta;   // per entry: 7 tapers
 };
 
 void d3_fany(const Step3Args& A, cudaStream_t st);
 void d3_flags(const Step3Args& A, cudaStream_t st);
-void d3_rhs(const Step3Args& A, cudaStream_t st);
+void d3_rhs(const Step3Args& A, cudaStream_t st);  // base (all nodes) + transfers (patch nodes)
 void d3_accumulate(const Step3Args& A, cudaStream_t st);
 
 struct Glob3Args {
