@@ -432,10 +432,17 @@ __device__ __forceinline__ Mem<MG> members(const Solve3Args& A) {
 }
 }  // namespace
 
+// Programmatic dependent launch (on by default; HDDM3_PDL=0 off): a solve kernel lets
+// its successor launch at once and waits for its predecessor before touching a vector.
+__device__ __forceinline__ void pdl_trigger3() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait3() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // shell (identity rows): x = b
 template <int MG>
 __global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_ring(Solve3Args A) {
+  pdl_trigger3();
   const Mem<MG> m = members<MG>(A);
+  pdl_wait3();
   for (int k = 0; k < m.cnt; ++k) {
     const long long o = (long long)m.t[k] * A.nw;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.nshell; i += gridDim.x * blockDim.x)
@@ -446,7 +453,9 @@ __global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_ring(Solve3Args A) {
 // forward assembly of the own entries: Y = b + the children's update vectors
 template <int MG>
 __global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_fasm(Solve3Args A, const Task3* tk) {
+  pdl_trigger3();
   const Mem<MG> m = members<MG>(A);
+  pdl_wait3();
   if (!m.cnt) return;
   const Task3 T = tk[blockIdx.x];
   const int i = T.a + threadIdx.x;
@@ -490,7 +499,9 @@ __device__ __forceinline__ void col_sweep(const Mem<MG>& m, const cplx* const* v
 template <int MG>
 __global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_fdiag(Solve3Args A, const Task3* tk, int nbig) {
   __shared__ cplx part[8][MG][32];
+  pdl_trigger3();
   const Mem<MG> m = members<MG>(A);
+  pdl_wait3();
   if (!m.cnt) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const bool big = int(blockIdx.x) < nbig;
@@ -533,7 +544,9 @@ __global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_fdiag(Solve3Args A, 
 template <int MG>
 __global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_fpanel(Solve3Args A, const Task3* tk, int nbig) {
   __shared__ cplx part[8][MG][32];
+  pdl_trigger3();
   const Mem<MG> m = members<MG>(A);
+  pdl_wait3();
   if (!m.cnt) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const bool big = int(blockIdx.x) < nbig;
@@ -579,7 +592,9 @@ __global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_fpanel(Solve3Args A,
 // backward gather of the ancestors' solution at the supernode's rows into U
 template <int MG>
 __global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_bgather(Solve3Args A, const Task3* tk) {
+  pdl_trigger3();
   const Mem<MG> m = members<MG>(A);
+  pdl_wait3();
   if (!m.cnt) return;
   const Task3 T = tk[blockIdx.x];
   const int k = T.a + threadIdx.x;
@@ -594,7 +609,9 @@ __global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_bgather(Solve3Args A
 template <int MG>
 __global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_bpanel(Solve3Args A, const Task3* tk, int nbig) {
   __shared__ cplx part[8][MG][32];
+  pdl_trigger3();
   const Mem<MG> m = members<MG>(A);
+  pdl_wait3();
   if (!m.cnt) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const bool big = int(blockIdx.x) < nbig;
@@ -639,7 +656,9 @@ __global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_bpanel(Solve3Args A,
 template <int MG>
 __global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_bdiag(Solve3Args A, const Task3* tk, int nbig) {
   __shared__ cplx part[8][MG][32];
+  pdl_trigger3();
   const Mem<MG> m = members<MG>(A);
+  pdl_wait3();
   if (!m.cnt) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const bool big = int(blockIdx.x) < nbig;
@@ -676,33 +695,48 @@ __global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_bdiag(Solve3Args A, 
   }
 }
 
+// measured 4.552 -> 4.517 ms per config-5 solve; HDDM3_PDL=0 switches it off
+static bool g_pdl3 = !(std::getenv("HDDM3_PDL") && std::getenv("HDDM3_PDL")[0] == '0');
+template <typename... KArgs, typename... Args>
+static void launch3(void (*k)(KArgs...), dim3 grid, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl3 ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, args...);
+}
 template <int MG>
 static void s3t_ring(const Solve3Args& A, int ncls, int ng, cudaStream_t st) {
-  k3s_ring<MG><<<dim3(std::max(1, std::min(64, (A.nshell + 255) / 256)), ncls, ng), 256, 0, st>>>(A);
+  launch3(k3s_ring<MG>, dim3(std::max(1, std::min(64, (A.nshell + 255) / 256)), ncls, ng), st, A);
 }
 template <int MG>
 static void s3t_fasm(const Solve3Args& A, const Task3* t, int nt, int ncls, int ng, cudaStream_t st) {
-  if (nt) k3s_fasm<MG><<<dim3(nt, ncls, ng), 256, 0, st>>>(A, t);
+  if (nt) launch3(k3s_fasm<MG>, dim3(nt, ncls, ng), st, A, t);
 }
 template <int MG>
 static void s3t_fdiag(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ng, cudaStream_t st) {
-  if (nt) k3s_fdiag<MG><<<dim3(nbig + (nt - nbig + 7) / 8, ncls, ng), 256, 0, st>>>(A, t, nbig);
+  if (nt) launch3(k3s_fdiag<MG>, dim3(nbig + (nt - nbig + 7) / 8, ncls, ng), st, A, t, nbig);
 }
 template <int MG>
 static void s3t_fpanel(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ng, cudaStream_t st) {
-  if (nt) k3s_fpanel<MG><<<dim3(nbig + (nt - nbig + 7) / 8, ncls, ng), 256, 0, st>>>(A, t, nbig);
+  if (nt) launch3(k3s_fpanel<MG>, dim3(nbig + (nt - nbig + 7) / 8, ncls, ng), st, A, t, nbig);
 }
 template <int MG>
 static void s3t_bgather(const Solve3Args& A, const Task3* t, int nt, int ncls, int ng, cudaStream_t st) {
-  if (nt) k3s_bgather<MG><<<dim3(nt, ncls, ng), 256, 0, st>>>(A, t);
+  if (nt) launch3(k3s_bgather<MG>, dim3(nt, ncls, ng), st, A, t);
 }
 template <int MG>
 static void s3t_bpanel(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ng, cudaStream_t st) {
-  if (nt) k3s_bpanel<MG><<<dim3(nbig + (nt - nbig + 7) / 8, ncls, ng), 256, 0, st>>>(A, t, nbig);
+  if (nt) launch3(k3s_bpanel<MG>, dim3(nbig + (nt - nbig + 7) / 8, ncls, ng), st, A, t, nbig);
 }
 template <int MG>
 static void s3t_bdiag(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ng, cudaStream_t st) {
-  if (nt) k3s_bdiag<MG><<<dim3(nbig + (nt - nbig + 7) / 8, ncls, ng), 256, 0, st>>>(A, t, nbig);
+  if (nt) launch3(k3s_bdiag<MG>, dim3(nbig + (nt - nbig + 7) / 8, ncls, ng), st, A, t, nbig);
 }
 
 
