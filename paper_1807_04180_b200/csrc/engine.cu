@@ -825,6 +825,58 @@ void hddm_engine::build_plan() {
     chunks4(plan.bwd_leafcol, ls);
   }
   std::vector<SegRec> fseg;  // forward run segments of every level's rows
+  // member-tile tensor-core pulls: 8-row blocks of each separator, the union of their
+  // run segments by source supernode (kernels.cuh MmaSeg)
+  std::vector<int> snof(Y.n, -1);
+  for (int s = 0; s < nsn; ++s)
+    for (int i = 0; i < Y.sn[s].n; ++i) snof[Y.sn[s].c0 + i] = s;
+  auto mma_tables = [&](SolveLevel& L, const std::vector<int2>& items, const std::vector<int4>& rec,
+                        const std::vector<SegRec>& segs) {
+    std::vector<int4> blks;
+    std::vector<MmaSeg> ms;
+    double padded = 0, stored = 0;
+    size_t k = 0;
+    while (k < items.size()) {
+      size_t e = k;
+      while (e < items.size() && items[e].x == items[k].x && e - k < 8) ++e;
+      std::map<int, std::pair<int, int>> uni;
+      for (size_t r = k; r < e; ++r)
+        for (int q = rec[r].y; q < rec[r].y + rec[r].z; ++q) {
+          const SegRec& g = segs[q];
+          const int src = snof[g.zb];
+          auto it = uni.find(src);
+          if (it == uni.end())
+            uni[src] = {g.zb, g.zb + g.len};
+          else
+            it->second = {std::min(it->second.first, g.zb), std::max(it->second.second, g.zb + g.len)};
+        }
+      blks.push_back(make_int4(int(k), int(e - k), int(ms.size()), int(uni.size())));
+      for (const auto& kv : uni) padded += double(kv.second.second - kv.second.first) * double(e - k);
+      for (size_t r = k; r < e; ++r)
+        for (int q = rec[r].y; q < rec[r].y + rec[r].z; ++q) stored += segs[q].len;
+      for (const auto& kv : uni) {
+        MmaSeg S = {};
+        S.zmin = kv.second.first;
+        S.ulen = kv.second.second - kv.second.first;
+        for (size_t r = k; r < e; ++r)
+          for (int q = rec[r].y; q < rec[r].y + rec[r].z; ++q) {
+            const SegRec& g = segs[q];
+            if (snof[g.zb] != kv.first) continue;
+            S.lo[r - k] = g.zb;
+            S.hi[r - k] = g.zb + g.len;
+            S.vb[r - k] = g.off - g.zb;
+          }
+        ms.push_back(S);
+      }
+      k = e;
+    }
+    L.nmblk = int(blks.size());
+    L.mma_fill = stored > 0 ? padded / stored : 0;
+    if (L.nmblk) {
+      L.d_mblk = upload(blks);
+      L.d_mseg = upload(ms);
+    }
+  };
   for (int h = 1; h <= Y.max_height; ++h) {
     std::vector<int2> v;
     for (int s = 0; s < nsn; ++s)
@@ -849,6 +901,7 @@ void hddm_engine::build_plan() {
     L.d_rec = upload(rec);
     L.avg_run = tot / long(v.size());
     L.avg_diag = dtot / long(v.size());
+    mma_tables(L, v, rec, fseg);
     plan.fwd.push_back(L);
   }
   std::vector<SegRec> fseg_sp;
@@ -902,6 +955,7 @@ void hddm_engine::build_plan() {
         F.d_rec = upload(rec);
         F.avg_run = tot / long(keep.size());
         F.avg_diag = dtot / long(keep.size());
+        mma_tables(F, keep, rec, fseg_sp);
       }
       plan.fwd_sp.push_back(F);
     }

@@ -62,8 +62,24 @@ struct TileArg {
 // One level of the level-synchronous sweeps: output items that are independent
 // given the previous levels -- rows (supernode, row) / leaves (leaf, 0) forward,
 // columns (supernode, column) backward.
+// Forward pulls of member tiles on the FP64 tensor cores: the level's rows in blocks
+// of up to 8 rows of one separator; per block the union of the rows' run segments by
+// source supernode (columns [zmin, zmin + ulen)), each row's piece of it
+// [lo, hi) with its values at vals[vb + z] (zero elsewhere: padding)
+struct MmaSeg {
+  int zmin, ulen;
+  int lo[8], hi[8];
+  long long vb[8];
+};
+
 struct SolveLevel {
   int nitem = 0;
+  // member-tile forward pulls by DMMA (k_fwd_pull_mma): blocks (first item, rows,
+  // first segment, segments)
+  int nmblk = 0;
+  int4* d_mblk = nullptr;
+  MmaSeg* d_mseg = nullptr;
+  double mma_fill = 0;  // padded / stored entries of the blocks
   int2* d_items = nullptr;
   int4* d_rec = nullptr;    // forward rows: (position, first segment, segment count, -)
   long avg_run = 0;         // forward: mean incoming run length

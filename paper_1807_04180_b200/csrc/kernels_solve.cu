@@ -298,6 +298,165 @@ __global__ void __launch_bounds__(kThreads) k_fwd_pull(SolveArgs A, TileArg T, c
   }
 }
 
+// separator rows of member tiles, forward pull on the FP64 tensor cores:
+// Y[r][k] = B[r][k] - sum_z L[r][z] X[z][k] for a block of up to 8 rows r of one
+// separator and the tile's members k (n-blocks of 8), as mma.sync m8n8k4 f64
+// (A = 8 rows x 4 columns of L, zero outside each row's run piece; B = 4 columns x 8
+// members of X, contiguous in the member-interleaved layout; complex products as four
+// real MMAs). A warp per (tile, block); the members' X of a column is read once per
+// block instead of once per row (the L2 re-reads of the lane-per-member kernel).
+__device__ __forceinline__ void dmma2(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int NB>
+__global__ void __launch_bounds__(256) k_fwd_pull_mma(SolveArgs A, TileArg T, const int4* __restrict__ rec,
+                                                      const int4* __restrict__ blk, const MmaSeg* __restrict__ segs,
+                                                      int nblk) {
+  // CTA per (tile, block); the 8 warps split the k-steps (interleaved), their partial
+  // accumulators combined in warp order
+  __shared__ double part[8][32][NB * 4];
+  pdl_trigger();
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int ti = blockIdx.x / nblk;
+  const int b = blockIdx.x - ti * nblk;
+  pdl_wait();
+  const TileRec* tr = T.rec + ti;
+  const int M = T.M, m = tr->m;
+  const long long cb = tr->cb;
+  bool any = false;  // a tile without an active member does nothing (CTA-uniform)
+  for (int k = 0; k < M; ++k) any |= (A.flag[tr->t[k]] != 0) == (A.flag_on != 0);
+  if (!any) return;
+  const int4 B = blk[b];  // (first item, rows, first segment, segments)
+  const int g = lane >> 2, q = lane & 3;
+  const cplx* vals = A.vals + (long long)tr->c * A.nvals;
+  const cplx* X = A.X + cb;
+  double cr[NB][2], ci[NB][2];
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb) cr[nb][0] = cr[nb][1] = ci[nb][0] = ci[nb][1] = 0.0;
+  for (int u = B.z; u < B.z + B.w; ++u) {
+    const MmaSeg& S = segs[u];
+    const int zmin = S.zmin, ulen = S.ulen;
+    const int lo = g < B.y ? S.lo[g] : 0, hi = g < B.y ? S.hi[g] : 0;
+    const cplx* vrow = vals + (g < B.y ? S.vb[g] : 0);
+    for (int k0 = 4 * wp; k0 < ulen; k0 += 32) {
+      const int z = zmin + k0 + q;
+      const bool zin = k0 + q < ulen;
+      const cplx a = (z >= lo && z < hi) ? ldf(vrow + z) : cmk(0, 0);
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) {
+        const int mem = nb * 8 + g;
+        const cplx x = (zin && mem < M) ? X[(long long)z * m + mem] : cmk(0, 0);
+        dmma2(cr[nb][0], cr[nb][1], a.x, x.x);
+        dmma2(cr[nb][0], cr[nb][1], -a.y, x.y);
+        dmma2(ci[nb][0], ci[nb][1], a.x, x.y);
+        dmma2(ci[nb][0], ci[nb][1], a.y, x.x);
+      }
+    }
+  }
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb) {
+    part[wp][lane][nb * 4 + 0] = cr[nb][0];
+    part[wp][lane][nb * 4 + 1] = cr[nb][1];
+    part[wp][lane][nb * 4 + 2] = ci[nb][0];
+    part[wp][lane][nb * 4 + 3] = ci[nb][1];
+  }
+  __syncthreads();
+  if (wp != 0 || g >= B.y) return;
+  double sum[NB * 4];
+#pragma unroll
+  for (int v = 0; v < NB * 4; ++v) {
+    double acc = part[0][lane][v];
+    for (int k = 1; k < 8; ++k) acc += part[k][lane][v];
+    sum[v] = acc;
+  }
+  const int pos = __ldg(rec + B.x + g).x;
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int mem = nb * 8 + 2 * q + h;
+      if (mem >= M) continue;
+      const long long p = cb + (long long)pos * m + mem;
+      A.Y[p] = csub(A.B[p], cmk(sum[nb * 4 + h], sum[nb * 4 + 2 + h]));
+    }
+}
+
+// separator rows of member tiles, forward dense inverse on the FP64 tensor cores:
+// X[i][k] = Y[i][k] + sum_{j<i} Linv[i][j] Y[j][k] for a block of up to 8 rows i of one
+// separator (the pull's row blocks), CTA per (tile, block), 8 warps splitting the
+// k-steps, combined in warp order.
+template <int NB>
+__global__ void __launch_bounds__(256) k_fwd_diag_mma(SolveArgs A, TileArg T, const int2* __restrict__ items,
+                                                      const int4* __restrict__ blk, int nblk) {
+  __shared__ double part[8][32][NB * 4];
+  pdl_trigger();
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int ti = blockIdx.x / nblk;
+  const int b = blockIdx.x - ti * nblk;
+  pdl_wait();
+  const TileRec* tr = T.rec + ti;
+  const int M = T.M, m = tr->m;
+  const long long cb = tr->cb;
+  bool any = false;
+  for (int k = 0; k < M; ++k) any |= (A.flag[tr->t[k]] != 0) == (A.flag_on != 0);
+  if (!any) return;
+  const int4 B = blk[b];
+  const int2 it0 = items[B.x];
+  const DevSn sn = A.sn[it0.x];
+  const int i0 = it0.y;
+  const int g = lane >> 2, q = lane & 3;
+  const int i = i0 + g;
+  const cplx* Linv = A.vals + (long long)tr->c * A.nvals + sn.diag_off;
+  const cplx* lrow = Linv + (long long)i * (i - 1) / 2;
+  const cplx* Yb = A.Y + cb + (long long)sn.c0 * m;
+  double cr[NB][2], ci[NB][2];
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb) cr[nb][0] = cr[nb][1] = ci[nb][0] = ci[nb][1] = 0.0;
+  const int jend = i0 + B.y - 1;  // columns below the block's last row
+  for (int k0 = 4 * wp; k0 < jend; k0 += 32) {
+    const int j = k0 + q;
+    const cplx a = (g < B.y && j < i) ? ldf(lrow + j) : cmk(0, 0);
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+      const int mem = nb * 8 + g;
+      const cplx x = (j < jend && mem < M) ? Yb[(long long)j * m + mem] : cmk(0, 0);
+      dmma2(cr[nb][0], cr[nb][1], a.x, x.x);
+      dmma2(cr[nb][0], cr[nb][1], -a.y, x.y);
+      dmma2(ci[nb][0], ci[nb][1], a.x, x.y);
+      dmma2(ci[nb][0], ci[nb][1], a.y, x.x);
+    }
+  }
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb) {
+    part[wp][lane][nb * 4 + 0] = cr[nb][0];
+    part[wp][lane][nb * 4 + 1] = cr[nb][1];
+    part[wp][lane][nb * 4 + 2] = ci[nb][0];
+    part[wp][lane][nb * 4 + 3] = ci[nb][1];
+  }
+  __syncthreads();
+  if (wp != 0 || g >= B.y) return;
+  double sum[NB * 4];
+#pragma unroll
+  for (int v = 0; v < NB * 4; ++v) {
+    double acc = part[0][lane][v];
+    for (int k = 1; k < 8; ++k) acc += part[k][lane][v];
+    sum[v] = acc;
+  }
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int mem = nb * 8 + 2 * q + h;
+      if (mem >= M) continue;
+      if ((A.flag[tr->t[mem]] != 0) != (A.flag_on != 0)) continue;
+      const long long p = cb + (long long)(sn.c0 + i) * m + mem;
+      A.X[p] = cadd(A.Y[p], cmk(sum[nb * 4 + h], sum[nb * 4 + 2 + h]));
+    }
+}
+
 // separator rows, forward diagonal: X[i] = Y[i] + sum_{j<i} Linv[i][j] Y[j]
 __global__ void __launch_bounds__(kThreads) k_fwd_diag(SolveArgs A, TileArg T, const int2* items,
                                                        int nitem) {
@@ -871,7 +1030,22 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
       continue;
     }
     const int li = int(&L - (sp ? P.fwd_sp.data() : P.fwd.data()));
-    if (!(skip & 4)) {
+    // member tiles: the tensor-core pull (HDDM_MMA_PULL=0: the lane-per-member kernel)
+    // on levels whose 8-row blocks pad the runs by at most HDDM_MMA_FILL
+    static const bool mma_pull = !(std::getenv("HDDM_MMA_PULL") && std::getenv("HDDM_MMA_PULL")[0] == '0');
+    static const double mma_fill = std::getenv("HDDM_MMA_FILL") ? std::atof(std::getenv("HDDM_MMA_FILL")) : 1.3;
+    // the dense-inverse rows on the tensor cores for separators with long rows only
+    static const long mma_diag_min = std::getenv("HDDM_MMA_DIAG_MIN") ? std::atol(std::getenv("HDDM_MMA_DIAG_MIN")) : 32;
+    if (skip & 4) {
+    } else if (mma_pull && T1.M >= 2 && T1.M <= 16 && L.nmblk > 0 && L.mma_fill <= mma_fill) {
+      const unsigned g = unsigned(nt * L.nmblk);  // CTA per (tile, block)
+      if (T1.M <= 8)
+        launch_pdl(k_fwd_pull_mma<1>, g, 256, 0, st, A, T1, (const int4*)L.d_rec, (const int4*)L.d_mblk,
+                   (const MmaSeg*)L.d_mseg, L.nmblk);
+      else
+        launch_pdl(k_fwd_pull_mma<2>, g, 256, 0, st, A, T1, (const int4*)L.d_rec, (const int4*)L.d_mblk,
+                   (const MmaSeg*)L.d_mseg, L.nmblk);
+    } else {
       const TileArg Tp = with_shape(T1, fwd_shape(T1.M, L.avg_run, false, sp, li));
       launch_pdl(k_fwd_pull, blocks(L.nitem, Tp.R), kThreads, 0, st, A, Tp, (const int4*)L.d_rec,
                  L.nitem);
@@ -879,6 +1053,14 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
     if (skip & 8) {
     } else if (A.lss && L.nsep > 0 && T1.M >= subst_min_m && T1.M <= 16) {
       launch_sep_trsv<false>(A, T1, L, st);
+    } else if (mma_pull && T1.M >= 2 && T1.M <= 16 && L.nmblk > 0 && L.avg_diag >= mma_diag_min) {
+      const unsigned g = unsigned(nt * L.nmblk);
+      if (T1.M <= 8)
+        launch_pdl(k_fwd_diag_mma<1>, g, 256, 0, st, A, T1, (const int2*)L.d_items, (const int4*)L.d_mblk,
+                   L.nmblk);
+      else
+        launch_pdl(k_fwd_diag_mma<2>, g, 256, 0, st, A, T1, (const int2*)L.d_items, (const int4*)L.d_mblk,
+                   L.nmblk);
     } else {
       const TileArg Td = with_shape(T1, fwd_shape(T1.M, L.avg_diag, true, sp, li));
       launch_pdl(k_fwd_diag, blocks(L.nitem, Td.R), kThreads, 0, st, A, Td, (const int2*)L.d_items,
