@@ -1000,6 +1000,20 @@ void hddm_engine::build_plan() {
     if (v.empty()) continue;
     SolveLevel L = level(v);
     chunks4(L, sns);
+    {  // member-tile tensor-core kernels: blocks of up to 8 columns of one separator
+      std::vector<int4> blks;
+      long dsum = 0;
+      for (size_t k = 0; k < v.size();) {
+        size_t e = k;
+        while (e < v.size() && v[e].x == v[k].x && e - k < 8) ++e;
+        blks.push_back(make_int4(int(k), int(e - k), 0, 0));
+        k = e;
+      }
+      for (const int2& it : v) dsum += Y.sn[it.x].n - 1 - it.y;
+      L.avg_diag = dsum / long(v.size());
+      L.nmblk = int(blks.size());
+      L.d_mblk = upload(blks);
+    }
     L.split_rows = rows > 64L * long(sns.size());  // long row lists
     L.split_diag = nmax > 48;
     if (env_sr) L.split_rows = std::atoi(env_sr) != 0;

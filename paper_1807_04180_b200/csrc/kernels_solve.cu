@@ -497,6 +497,108 @@ __global__ void __launch_bounds__(kThreads) k_fwd_diag(SolveArgs A, TileArg T, c
   }
 }
 
+// Member tiles' backward on the FP64 tensor cores, blocks of up to 8 columns j of one
+// separator (lane group g = column), CTA per (tile, block), the 8 warps splitting the
+// k-steps, partials combined in warp order:
+//   pull:    Y[j][k] = Dinv_j z_j[k] - sum_r L[r][j] X[dst r][k] over the rows reaching
+//            the block (a prefix of the first-column-sorted list; zero left of a row's
+//            first column);
+//   inverse: X[j][k] = Y[j][k] + sum_{i>j} Linv[i][j] Y[i][k].
+template <int NB, bool DIAG>
+__global__ void __launch_bounds__(256) k_bwd_mma(SolveArgs A, TileArg T, const int2* __restrict__ items,
+                                                 const int4* __restrict__ blk, int nblk) {
+  __shared__ double part[8][32][NB * 4];
+  pdl_trigger();
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int ti = blockIdx.x / nblk;
+  const int b = blockIdx.x - ti * nblk;
+  pdl_wait();
+  const TileRec* tr = T.rec + ti;
+  const int M = T.M, m = tr->m;
+  const long long cb = tr->cb;
+  bool any = false;
+  for (int k = 0; k < M; ++k) any |= (A.flag[tr->t[k]] != 0) == (A.flag_on != 0);
+  if (!any) return;
+  const int4 B = blk[b];
+  const int2 it0 = items[B.x];
+  const DevSn sn = A.sn[it0.x];
+  const int j0 = it0.y;
+  const int g = lane >> 2, q = lane & 3;
+  const int j = j0 + g;
+  const bool col = g < B.y;
+  const cplx* vals = A.vals + (long long)tr->c * A.nvals;
+  double cr[NB][2], ci[NB][2];
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb) cr[nb][0] = cr[nb][1] = ci[nb][0] = ci[nb][1] = 0.0;
+  if (DIAG) {
+    const cplx* Linv = vals + sn.diag_off;
+    const cplx* Yb = A.Y + cb + (long long)sn.c0 * m;
+    for (int i0 = j0 + 1 + 4 * wp; i0 < sn.n; i0 += 32) {
+      // A: rows = the block's columns j (lane group g), k = rows i of Linv (lane q)
+      const int ia = i0 + q;  // the Linv row this lane loads for its column j
+      const cplx a = (col && ia < sn.n && ia > j) ? ldf(Linv + (long long)ia * (ia - 1) / 2 + j) : cmk(0, 0);
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) {
+        const int mem = nb * 8 + g;
+        const cplx x = (ia < sn.n && mem < M) ? Yb[(long long)ia * m + mem] : cmk(0, 0);
+        dmma2(cr[nb][0], cr[nb][1], a.x, x.x);
+        dmma2(cr[nb][0], cr[nb][1], -a.y, x.y);
+        dmma2(ci[nb][0], ci[nb][1], a.x, x.y);
+        dmma2(ci[nb][0], ci[nb][1], a.y, x.x);
+      }
+    }
+  } else {
+    const BwRow* rows = A.bw + A.bw_ptr[it0.x];
+    const int nr = rows_upto(rows, A.bw_ptr[it0.x + 1] - A.bw_ptr[it0.x], j0 + B.y - 1);
+    const cplx* Xb = A.X + cb;
+    for (int r0 = 4 * wp; r0 < nr; r0 += 32) {
+      const int rk = r0 + q;
+      const BwRow d = rk < nr ? rows[rk] : BwRow{0, 1 << 30, 0};
+      const cplx a = (col && j >= d.first) ? ldf(vals + d.off + (j - d.first)) : cmk(0, 0);
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) {
+        const int mem = nb * 8 + g;
+        const cplx x = (rk < nr && mem < M) ? Xb[(long long)d.dpos * m + mem] : cmk(0, 0);
+        dmma2(cr[nb][0], cr[nb][1], a.x, x.x);
+        dmma2(cr[nb][0], cr[nb][1], -a.y, x.y);
+        dmma2(ci[nb][0], ci[nb][1], a.x, x.y);
+        dmma2(ci[nb][0], ci[nb][1], a.y, x.x);
+      }
+    }
+  }
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb) {
+    part[wp][lane][nb * 4 + 0] = cr[nb][0];
+    part[wp][lane][nb * 4 + 1] = cr[nb][1];
+    part[wp][lane][nb * 4 + 2] = ci[nb][0];
+    part[wp][lane][nb * 4 + 3] = ci[nb][1];
+  }
+  __syncthreads();
+  if (wp != 0 || !col) return;
+  double sum[NB * 4];
+#pragma unroll
+  for (int v = 0; v < NB * 4; ++v) {
+    double acc = part[0][lane][v];
+    for (int k = 1; k < 8; ++k) acc += part[k][lane][v];
+    sum[v] = acc;
+  }
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int mem = nb * 8 + 2 * q + h;
+      if (mem >= M) continue;
+      const long long p = cb + (long long)(sn.c0 + j) * m + mem;
+      const cplx s2 = cmk(sum[nb * 4 + h], sum[nb * 4 + 2 + h]);
+      if (DIAG) {
+        if ((A.flag[tr->t[mem]] != 0) != (A.flag_on != 0)) continue;
+        A.X[p] = cadd(A.Y[p], s2);
+      } else {
+        A.Y[p] = csub(cmul(ldg(vals + sn.dinv_off + j), zval(A, it0.x, p)), s2);
+      }
+    }
+}
+
 // backward pull, thread per (column, member) (T.E == 1; items are columns):
 // w_j = Dinv[j] X[j] - sum_rows L[r][j] X[dst r] into Y (in place into X for leaf
 // columns). Rows are sorted by first stored column: column j walks only the
@@ -1077,7 +1179,18 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
         std::getenv("HDDM_STAGE_MIN_M") ? std::atoi(std::getenv("HDDM_STAGE_MIN_M")) : 2;
     const bool staged = P.staged && T1.M >= stage_min_m;
     const bool use_sub = staged && TS.ntile > 0 && (long long)T1.ntile * L.nchunk4 < P.sub_bwd_ctas;
+    static const bool mma_bwd = !(std::getenv("HDDM_MMA_BWD") && std::getenv("HDDM_MMA_BWD")[0] == '0');
+    const bool mma_ok = mma_bwd && T1.M >= 2 && T1.M <= 16 && L.nmblk > 0;
+    const unsigned gm = unsigned(nt * L.nmblk);
+    // the pulls stay on the staged kernel (measured: the tensor-core pull 1.699 -> 1.731 ms
+    // per config-4 step); HDDM_MMA_BPULL=1 selects it
+    static const bool mma_bpull = std::getenv("HDDM_MMA_BPULL") && std::getenv("HDDM_MMA_BPULL")[0] == '1';
     if (skip & 16) {
+    } else if (mma_ok && mma_bpull) {
+      if (T1.M <= 8)
+        launch_pdl(k_bwd_mma<1, false>, gm, 256, 0, st, A, T1, (const int2*)L.d_items, (const int4*)L.d_mblk, L.nmblk);
+      else
+        launch_pdl(k_bwd_mma<2, false>, gm, 256, 0, st, A, T1, (const int2*)L.d_items, (const int4*)L.d_mblk, L.nmblk);
     } else if (staged)
       launch_bwd_stage<false>(A, use_sub ? with_shape(TS, 1) : T1, L, st);
     else if (L.split_rows && has_grp)
@@ -1086,9 +1199,16 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
     else
       launch_pdl(k_bwd_pull<false>, blocks(L.nitem, T1.R), kThreads, 0, st, A, T1,
                  (const int2*)L.d_items, L.nitem);
+    static const long mma_bdiag_min =
+        std::getenv("HDDM_MMA_DIAG_MIN") ? std::atol(std::getenv("HDDM_MMA_DIAG_MIN")) : 32;
     if (skip & 32) {
     } else if (A.lss && L.nsep > 0 && T1.M >= subst_min_m && T1.M <= 16) {
       launch_sep_trsv<true>(A, T1, L, st);
+    } else if (mma_ok && L.avg_diag >= mma_bdiag_min) {
+      if (T1.M <= 8)
+        launch_pdl(k_bwd_mma<1, true>, gm, 256, 0, st, A, T1, (const int2*)L.d_items, (const int4*)L.d_mblk, L.nmblk);
+      else
+        launch_pdl(k_bwd_mma<2, true>, gm, 256, 0, st, A, T1, (const int2*)L.d_items, (const int4*)L.d_mblk, L.nmblk);
     } else if (L.split_diag && has_grp)
       launch_pdl(k_bwd_split<true>, gs, kSplitWarps * 32, 0, st, A, T1, (const int2*)grp->second.second,
                  grp->second.first);
