@@ -136,7 +136,9 @@ def barrier(world: int):
 def solve_traffic(cfg: int):
     """Solve-stage DRAM bytes per solve from the committed ncu step summary of this
     config (profiles/r02_step_summary_cfg<N>.json, tools/ncu_step.py)."""
-    path = os.path.join(ROOT, "profiles", f"r02_step_summary_cfg{cfg}.json")
+    path = os.path.join(ROOT, "profiles", f"r02_final_step_summary_cfg{cfg}.json")
+    if not os.path.exists(path):
+        path = os.path.join(ROOT, "profiles", f"r02_step_summary_cfg{cfg}.json")
     try:
         with open(path) as f:
             return json.load(f)["solve_dram_bytes"]
@@ -472,8 +474,8 @@ def run_ours(args, world, rank, local):
                          "frac": (achieved / peak) if achieved else None,
                          "traffic": solve_traffic(args.config),
                          "traffic_note": "DRAM bytes of the solve-stage kernels of one step, "
-                                         f"profiles/r02_step_summary_cfg{args.config}.json (ncu "
-                                         "launch list, cache flushed per launch: an upper bound)",
+                                         f"profiles/r02[_final]_step_summary_cfg{args.config}.json "
+                                         "(ncu launch list, cache flushed per launch: an upper bound)",
                          "kernel": "batched supernodal solve stage (fwd+bwd, all classes)",
                          "bytes_per_launch": B["B_solve"], "ms_per_launch": solve_ms_per,
                          "peak_kind": peak_kind},

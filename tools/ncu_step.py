@@ -8,7 +8,8 @@ import json
 import sys
 
 SOLVE = ("k_ring", "k_fwd_leaf", "k_fwd_pull", "k_fwd_diag", "k_bwd_stage", "k_bwd_pull",
-         "k_bwd_diag", "k_bwd_split", "k_bwd_leaf", "k_sep_trsv")
+         "k_bwd_diag", "k_bwd_split", "k_bwd_leaf", "k_sep_trsv", "k_fwd_pull_mma",
+         "k_fwd_diag_mma", "k_bwd_mma")
 
 
 def load(path):
