@@ -83,6 +83,7 @@ struct hddm3_engine {
     int n = 0, nbig = 0;
   };
   std::vector<Lvl> f_asm, f_diag, f_pan, b_gat, b_pan, b_diag;
+  Lvl f_leaf, b_leaf;  // fused leaf kernels (all leaves at most 32 nodes)
   // per subdomain
   Sub3Dev* d_sub = nullptr;
   cplx* d_cop = nullptr;
@@ -473,11 +474,24 @@ void hddm3_engine::build_plan() {
     big.insert(big.end(), small.begin(), small.end());
     return nbig;
   };
+  // leaves of at most 32 nodes: one fused warp kernel each way (k3s_fleaf / k3s_bleaf)
+  bool fuse = true;
+  for (int s = 0; s < nsn; ++s)
+    if (Y.sn[s].nch == 0 && Y.sn[s].n > 32) fuse = false;
+  if (fuse) {
+    std::vector<Task3> lf;
+    for (int s = 0; s < nsn; ++s)
+      if (Y.sn[s].nch == 0) lf.push_back(task(s, 0, Y.sn[s].n));
+    while (lf.size() % 8) lf.push_back(Task3{});
+    f_leaf = up(lf);
+    b_leaf = up(lf);
+  }
+  auto leaf = [&](int s) { return fuse && Y.sn[s].nch == 0; };
   for (int h = 0; h <= Y.max_height; ++h) {
     std::vector<Task3> a, db, ds, pb, ps;
     for (int s = 0; s < nsn; ++s) {
       const Sn3& x = Y.sn[s];
-      if (x.height != h) continue;
+      if (x.height != h || leaf(s)) continue;
       const int r = int(x.rows.size());
       const bool big = x.n > kSmallCols;
       for (int i = 0; i < x.n; i += 256) a.push_back(task(s, i, std::min(x.n, i + 256)));
@@ -494,7 +508,7 @@ void hddm3_engine::build_plan() {
     std::vector<Task3> g, pb, ps, db, ds;
     for (int s = 0; s < nsn; ++s) {
       const Sn3& x = Y.sn[s];
-      if (x.depth != dd) continue;
+      if (x.depth != dd || leaf(s)) continue;
       const int r = int(x.rows.size());
       for (int k = 0; k < r; k += 256) g.push_back(task(s, k, std::min(r, k + 256)));
       for (int j = 0; j < x.n; j += kColsPerTask) {
@@ -511,7 +525,7 @@ void hddm3_engine::build_plan() {
 }
 
 int hddm3_engine::solve_launches() const {
-  int n = 1;
+  int n = 1 + (f_leaf.n > 0) + (b_leaf.n > 0);
   for (size_t h = 0; h < f_asm.size(); ++h) n += (f_asm[h].n > 0) + (f_diag[h].n > 0) + (f_pan[h].n > 0);
   for (size_t d = 0; d < b_gat.size(); ++d) n += (b_gat[d].n > 0) + (b_pan[d].n > 0) + (b_diag[d].n > 0);
   return n;
@@ -587,6 +601,7 @@ Solve3Args hddm3_engine::solve_args(const cplx* B, cplx* X, const int* flag, int
 
 void hddm3_engine::enqueue_solve(const Solve3Args& A, cudaStream_t s) {
   s3_ring(A, ncls, ngroups, s);
+  s3_fleaf(A, f_leaf.d, f_leaf.n, ncls, ngroups, s);
   for (size_t h = 0; h < f_asm.size(); ++h) {
     s3_fasm(A, f_asm[h].d, f_asm[h].n, ncls, ngroups, s);
     s3_fdiag(A, f_diag[h].d, f_diag[h].n, f_diag[h].nbig, ncls, ngroups, s);
@@ -597,6 +612,7 @@ void hddm3_engine::enqueue_solve(const Solve3Args& A, cudaStream_t s) {
     s3_bpanel(A, b_pan[d].d, b_pan[d].n, b_pan[d].nbig, ncls, ngroups, s);
     s3_bdiag(A, b_diag[d].d, b_diag[d].n, b_diag[d].nbig, ncls, ngroups, s);
   }
+  s3_bleaf(A, b_leaf.d, b_leaf.n, ncls, ngroups, s);
 }
 
 Chk3Args hddm3_engine::chk_args(const cplx* B, cplx* X, const int* flag, int on, unsigned long long cond) {

@@ -438,6 +438,121 @@ __device__ __forceinline__ void pdl_trigger3() { asm volatile("griddepcontrol.la
 __device__ __forceinline__ void pdl_wait3() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // shell (identity rows): x = b
+// Leaves (no children, at most 32 nodes) fused, a warp per leaf, lane = node:
+//   forward:  x = Linv b (y_j broadcast by shuffles), then the panel rows
+//             u_k = -sum_j L_kj x_j (lane = row, x_j by shuffles): no assembly pass and
+//             no round trip between the two products;
+//   backward: w_j = z_j / d_j - sum_k L_kj x_rows(k) (the ancestors' x gathered
+//             directly), then x = Linv^T w (w_i by shuffles).
+template <int MG>
+__global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_fleaf(Solve3Args A, const Task3* tk) {
+  pdl_trigger3();
+  const Mem<MG> m = members<MG>(A);
+  pdl_wait3();
+  if (!m.cnt) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const Task3 T = tk[blockIdx.x * 8 + w];
+  if (T.b <= T.a) return;
+  const int n = T.n, r = T.r, i = lane;
+  const cplx* vals = A.vals + (long long)blockIdx.y * A.nvals;
+  const cplx* L = vals + T.linv;
+  cplx x[MG];
+#pragma unroll
+  for (int q = 0; q < MG; ++q) x[q] = (q < m.cnt && i < n) ? A.B[(long long)m.t[q] * A.nw + T.c0 + i] : cmk(0, 0);
+  cplx acc[MG];
+#pragma unroll
+  for (int q = 0; q < MG; ++q) acc[q] = x[q];
+  for (int j = 0; j + 1 < n; ++j) {
+    const cplx l = (i < n && j < i) ? ldf(L + colstart(j, n) + (i - j - 1)) : cmk(0, 0);
+#pragma unroll
+    for (int q = 0; q < MG; ++q) {
+      if (q >= m.cnt) break;
+      const cplx yj = cmk(__shfl_sync(0xffffffffu, x[q].x, j), __shfl_sync(0xffffffffu, x[q].y, j));
+      cfma(acc[q], l, yj);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < MG; ++q) {
+    if (q >= m.cnt) break;
+    x[q] = acc[q];
+    if (i < n) A.X[(long long)m.t[q] * A.nw + T.c0 + i] = x[q];
+  }
+  const cplx* P = vals + T.pan;
+  for (int k0 = 0; k0 < r; k0 += 32) {
+    const int k = k0 + lane;
+    cplx u[MG];
+#pragma unroll
+    for (int q = 0; q < MG; ++q) u[q] = cmk(0, 0);
+    for (int j = 0; j < n; ++j) {
+      const cplx l = k < r ? ldf(P + (long long)j * r + k) : cmk(0, 0);
+#pragma unroll
+      for (int q = 0; q < MG; ++q) {
+        if (q >= m.cnt) break;
+        const cplx xj = cmk(__shfl_sync(0xffffffffu, x[q].x, j), __shfl_sync(0xffffffffu, x[q].y, j));
+        cfma(u[q], l, xj);
+      }
+    }
+    if (k < r)
+#pragma unroll
+      for (int q = 0; q < MG; ++q) {
+        if (q >= m.cnt) break;
+        A.U[(long long)m.t[q] * A.nupd + T.upd + k] = cmk(-u[q].x, -u[q].y);
+      }
+  }
+}
+
+template <int MG>
+__global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_bleaf(Solve3Args A, const Task3* tk) {
+  pdl_trigger3();
+  const Mem<MG> m = members<MG>(A);
+  pdl_wait3();
+  if (!m.cnt) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const Task3 T = tk[blockIdx.x * 8 + w];
+  if (T.b <= T.a) return;
+  const int n = T.n, r = T.r, j = lane;
+  const bool col = j < n;
+  const cplx* valsT = A.valsT + (long long)blockIdx.y * A.nvals;
+  const cplx* PT = valsT + T.pan;
+  const int* rows = A.rows_all + T.rows;
+  cplx acc[MG];
+#pragma unroll
+  for (int q = 0; q < MG; ++q) acc[q] = cmk(0, 0);
+  for (int k = 0; k < r; ++k) {
+    const cplx l = col ? ldf(PT + (long long)k * n + j) : cmk(0, 0);
+    const int pr = rows[k];
+#pragma unroll
+    for (int q = 0; q < MG; ++q) {
+      if (q >= m.cnt) break;
+      cfma(acc[q], l, A.X[(long long)m.t[q] * A.nw + pr]);
+    }
+  }
+  const cplx d = A.vals[(long long)blockIdx.y * A.nvals + T.c0 + (col ? j : 0)];
+  cplx wv[MG];
+#pragma unroll
+  for (int q = 0; q < MG; ++q) {
+    wv[q] = cmk(0, 0);
+    if (q < m.cnt && col) wv[q] = csub(cdiv(A.X[(long long)m.t[q] * A.nw + T.c0 + j], d), acc[q]);
+    acc[q] = wv[q];
+  }
+  const cplx* LT = valsT + T.linv;
+  for (int i = 1; i < n; ++i) {
+    const cplx l = (col && i > j) ? ldf(LT + (long long)i * (i - 1) / 2 + j) : cmk(0, 0);
+#pragma unroll
+    for (int q = 0; q < MG; ++q) {
+      if (q >= m.cnt) break;
+      const cplx wi = cmk(__shfl_sync(0xffffffffu, wv[q].x, i), __shfl_sync(0xffffffffu, wv[q].y, i));
+      cfma(acc[q], l, wi);
+    }
+  }
+  if (!col) return;
+#pragma unroll
+  for (int q = 0; q < MG; ++q) {
+    if (q >= m.cnt) break;
+    A.X[(long long)m.t[q] * A.nw + T.c0 + j] = acc[q];
+  }
+}
+
 template <int MG>
 __global__ void __launch_bounds__(256, MG == 1 ? 4 : 3) k3s_ring(Solve3Args A) {
   pdl_trigger3();
@@ -727,6 +842,14 @@ static void s3t_fpanel(const Solve3Args& A, const Task3* t, int nt, int nbig, in
   if (nt) launch3(k3s_fpanel<MG>, dim3(nbig + (nt - nbig + 7) / 8, ncls, ng), st, A, t, nbig);
 }
 template <int MG>
+static void s3t_fleaf(const Solve3Args& A, const Task3* t, int nt, int ncls, int ng, cudaStream_t st) {
+  if (nt) launch3(k3s_fleaf<MG>, dim3(nt / 8, ncls, ng), st, A, t);
+}
+template <int MG>
+static void s3t_bleaf(const Solve3Args& A, const Task3* t, int nt, int ncls, int ng, cudaStream_t st) {
+  if (nt) launch3(k3s_bleaf<MG>, dim3(nt / 8, ncls, ng), st, A, t);
+}
+template <int MG>
 static void s3t_bgather(const Solve3Args& A, const Task3* t, int nt, int ncls, int ng, cudaStream_t st) {
   if (nt) launch3(k3s_bgather<MG>, dim3(nt, ncls, ng), st, A, t);
 }
@@ -756,6 +879,8 @@ void s3_ring(const Solve3Args& A, int ncls, int ng, cudaStream_t st) {
     else s3t_##name<kMG>(A, t, nt, nbig, ncls, ng, st);                                         \
   }
 S3_DISPATCH(fasm)
+S3_DISPATCH(fleaf)
+S3_DISPATCH(bleaf)
 S3_DISPATCH(bgather)
 S3_DISPATCH_B(fdiag)
 S3_DISPATCH_B(fpanel)

@@ -80,6 +80,9 @@ void s3_fasm(const Solve3Args& A, const Task3* t, int nt, int ncls, int ngroups,
 void s3_fdiag(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ngroups, cudaStream_t st);
 void s3_fpanel(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ngroups, cudaStream_t st);
 void s3_bgather(const Solve3Args& A, const Task3* t, int nt, int ncls, int ngroups, cudaStream_t st);
+// leaves (no children, <= 32 nodes), a warp per leaf; nt a multiple of 8
+void s3_fleaf(const Solve3Args& A, const Task3* t, int nt, int ncls, int ngroups, cudaStream_t st);
+void s3_bleaf(const Solve3Args& A, const Task3* t, int nt, int ncls, int ngroups, cudaStream_t st);
 void s3_bpanel(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ngroups, cudaStream_t st);
 void s3_bdiag(const Solve3Args& A, const Task3* t, int nt, int nbig, int ncls, int ngroups, cudaStream_t st);
 
