@@ -166,6 +166,8 @@ struct hddm_engine {
   int* d_pnode = nullptr;
   int* d_pmask = nullptr;
   int* d_xfer_pos = nullptr;
+  int4* d_xblk = nullptr;  // transfer block table (kernels.cuh StepArgs::xblk)
+  int nxblk = 0;
   int2* d_lpq = nullptr;    // residual-check tables (per factor position)
   int4* d_nbr = nullptr;
   double* d_k2c = nullptr;  // per class: window k^2 in factor order
@@ -634,6 +636,19 @@ void hddm_engine::create(const hddm_problem& p) {
     }
     d_xfer_pos = upload(xpos);
     d_xfer_beta = upload(xbeta);
+    // transfer blocks: member slabs of <= 32 per class, 256 / M patch nodes per block
+    std::vector<int4> xb;
+    for (int c = 0; c < ncls; ++c) {
+      const int m = S.cls_ptr[c + 1] - S.cls_ptr[c];
+      const int nslab = (m + 31) / 32;
+      for (int sl = 0; sl < nslab; ++sl) {
+        const int k0 = int((long long)m * sl / nslab), k1 = int((long long)m * (sl + 1) / nslab);
+        const int M = k1 - k0, per = 256 / M;
+        for (int u0 = 0; u0 < npatch; u0 += per) xb.push_back(make_int4(c, k0, M, u0));
+      }
+    }
+    nxblk = int(xb.size());
+    d_xblk = upload(xb);
   }
   // residual check tables (the J-scaled window stencil, discretize.cpp:98-160):
   // window coordinates and neighbour positions per factor position, k^2 per class
@@ -1225,6 +1240,9 @@ StepArgs hddm_engine::step_args(int s, const cplx* f) {
   A.pmask = d_pmask;
   A.xfer_pos = d_xfer_pos;
   A.xfer_beta = d_xfer_beta;
+  A.xblk = d_xblk;
+  A.nxblk = nxblk;
+  A.k2c = d_k2c;
   A.ih2 = 1.0 / (S.h * S.h);
   A.sub = d_sub;
   A.sa = d_sa;

@@ -169,6 +169,9 @@ struct StepArgs {
   const int* pmask;      // bit d: node lies in direction d's patch
   const int* xfer_pos;      // per (patch node, direction, stencil point): source position or -1
   const double* xfer_beta;  // ... and transfer_beta there
+  const int4* xblk;         // transfer blocks: (class, first member slot, members, first patch node)
+  int nxblk;
+  const double* k2c;        // per class: window k^2 in factor order
   double ih2;
   const DevSub* sub;
   const cplx* sa;        // per-sub alpha arrays: a1n[wnx] ia1h[wnx] a2n[wny] ia2h[wny]

@@ -140,27 +140,41 @@ __global__ void __launch_bounds__(256) k_rhs_base(StepArgs A) {
 #ifndef HDDM_XFER_MINB
 #define HDDM_XFER_MINB 3  // register cap for occupancy: measured -8% per step with the check
 #endif
+// Block table (StepArgs::xblk): block -> (class c, first member slot k0, members M <= 32,
+// first patch node u0). Thread tid serves member k0 + tid % M at patch node u0 + tid / M:
+// the members of a class at one position are adjacent in the interleaved layout, so a
+// warp's loads of a neighbour's solution and its stores of B are contiguous runs of M
+// values (sources of adjacent members are adjacent members of the source's class on a
+// regular partition), and the structural tables and the class coefficients are
+// broadcast loads. Members of a class have bitwise-identical window operators (the
+// class criterion), so alpha and k^2 come from the class representative.
 __global__ void __launch_bounds__(256, HDDM_XFER_MINB) k_rhs_transfer(StepArgs A) {
-  const int t = blockIdx.y;
+  const int4 blk = __ldg(A.xblk + blockIdx.x);
+  const int c = blk.x, M = blk.z;
+  const int pi = threadIdx.x / M;
+  const int u = blk.w + pi;
+  if (pi >= 256 / M || u >= A.npatch) return;
+  const int c0 = __ldg(A.vm.cptr + c);
+  const int t = __ldg(A.vm.cmem + c0 + blk.y + threadIdx.x % M);
   if (A.zc[t]) return;
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
-  if (u >= A.npatch) return;
-  const int node = A.pnode[u];
-  const int mask = A.pmask[u];
+  const int node = __ldg(A.pnode + u);
+  const int mask = __ldg(A.pmask + u);
+  const int tpos = __ldg(A.pinv + node);
   const int lp = node % A.wnx, lq = node / A.wnx;
   const DevSub T = A.sub[t];
-  const int P = T.wx0 + lp, Q = T.wy0 + lq;
-  const cplx* sa = A.sa + (long long)t * A.sa_stride;
+  const cplx* sa = A.sa + (long long)__ldg(A.vm.cmem + c0) * A.sa_stride;
   const cplx a1 = sa[lp], a2 = sa[2 * A.wnx + lq];
   const cplx ia1w = sa[A.wnx + lp - 1], ia1e = sa[A.wnx + lp];
   const cplx ia2s = sa[2 * A.wnx + A.wny + lq - 1], ia2n = sa[2 * A.wnx + A.wny + lq];
   const cplx jac = cmul(a1, a2);
-  const double k2 = A.k2[(long long)Q * A.gnx + P];
+  const double k2 = __ldg(A.k2c + (long long)c * A.nw + tpos);
   const cplx ex = cscale(a2, A.ih2), ey = cscale(a1, A.ih2);
   const cplx cE = cmul(ex, ia1e), cW = cmul(ex, ia1w), cN = cmul(ey, ia2n), cS = cmul(ey, ia2s);
   cplx val = cmk(0, 0);
-  if (A.step == 1 && P >= T.own0 && P <= T.own1 && Q >= T.own2 && Q <= T.own3)
-    val = A.f[(long long)Q * A.gnx + P];
+  if (A.step == 1) {
+    const int P = T.wx0 + lp, Q = T.wy0 + lq;
+    if (P >= T.own0 && P <= T.own1 && Q >= T.own2 && Q <= T.own3) val = A.f[(long long)Q * A.gnx + P];
+  }
   bool any = false;
   for (int d = 0; d < 8; ++d) {
     if (!((mask >> d) & 1)) continue;
@@ -196,14 +210,13 @@ __global__ void __launch_bounds__(256, HDDM_XFER_MINB) k_rhs_transfer(StepArgs A
   // write every patch node (0 without a contribution), so B stays zero off the
   // patches after the one clear at step 2
   if (any)
-    vview(A.B, A.vm, t)[A.pinv[node]] = cmul(jac, val);
+    vview(A.B, A.vm, t)[tpos] = cmul(jac, val);
   else if (A.step != 1)
-    vview(A.B, A.vm, t)[A.pinv[node]] = cmk(0, 0);
+    vview(A.B, A.vm, t)[tpos] = cmk(0, 0);
 }
 
 void launch_transfer(const StepArgs& A, cudaStream_t st) {
-  dim3 g2((A.npatch + 255) / 256, A.nsub);
-  k_rhs_transfer<<<g2, 256, 0, st>>>(A);
+  k_rhs_transfer<<<A.nxblk, 256, 0, st>>>(A);
 }
 
 void launch_gather(const StepArgs& A, cudaStream_t st) {
@@ -214,8 +227,7 @@ void launch_gather(const StepArgs& A, cudaStream_t st) {
     k_rhs_base<<<unsigned((A.vm.total + 255) / 256), 256, 0, st>>>(A);
   else if (A.step == 2)
     cudaMemsetAsync(A.B, 0, size_t(A.vm.total) * sizeof(cplx), st);
-  dim3 g2((A.npatch + 255) / 256, A.nsub);
-  k_rhs_transfer<<<g2, 256, 0, st>>>(A);
+  k_rhs_transfer<<<A.nxblk, 256, 0, st>>>(A);
 }
 
 // ------------------------------------------------------------ accumulate
