@@ -171,6 +171,8 @@ struct hddm_engine {
   int2* d_lpq = nullptr;    // residual-check tables (per factor position)
   int4* d_nbr = nullptr;
   double* d_k2c = nullptr;  // per class: window k^2 in factor order
+  cplx* d_ctab = nullptr;         // tabulated check coefficients of the member classes
+  long long* d_ctab_off = nullptr;
   double* d_xfer_beta = nullptr;
   int npatch = 0;
   int* d_rowcov = nullptr;
@@ -676,6 +678,23 @@ void hddm_engine::create(const hddm_problem& p) {
       }
     }
     d_k2c = upload(k2c);
+    // row coefficients tabulated for classes with >= HDDM_CTAB_MIN members (80 B per
+    // position and class; the members re-read them instead of re-forming them)
+    static const int ctab_min = std::getenv("HDDM_CTAB_MIN") ? std::atoi(std::getenv("HDDM_CTAB_MIN")) : 4;
+    std::vector<long long> off(ncls, -1);
+    long long tot = 0;
+    for (int c = 0; c < ncls; ++c)
+      if (S.cls_ptr[c + 1] - S.cls_ptr[c] >= ctab_min) {
+        off[c] = tot;
+        tot += (long long)nw * 5;
+      }
+    if (tot > 0) {
+      d_ctab = dalloc<cplx>(size_t(tot));
+      d_ctab_off = upload(off);
+      const CheckArgs C = check_args(nullptr, nullptr, nullptr, nullptr);
+      for (int c = 0; c < ncls; ++c)
+        if (off[c] >= 0) launch_build_ctab(C, c, d_ctab + off[c], st);
+    }
   }
   d_part = dalloc<double>(2 * size_t(reduce_blocks()));
   d_scal = dalloc<double>(64);
@@ -784,6 +803,7 @@ void hddm_engine::build_plan() {
         G.M = M;
         G.E = 1;
         G.R = 32 / M;
+        tile_mags(G);
         for (auto& t : part) {
           plan.tiles.push_back(t);
           plan.tile_group.push_back(int(plan.groups.size()));
@@ -830,7 +850,11 @@ void hddm_engine::build_plan() {
   plan.staged = std::getenv("HDDM_NO_STAGE") == nullptr;
   if (const char* v = std::getenv("HDDM_SUB_RUN")) plan.sub_run = std::atol(v);
   if (const char* v = std::getenv("HDDM_SUB_BWD")) plan.sub_bwd_ctas = std::atoi(v);
-  set_solve_pdl(std::getenv("HDDM_PDL") != nullptr);  // measured slower at config 4: opt-in
+  // programmatic dependent launch of the level chains: measured faster only when every
+  // class is a singleton (config 3: 1.909 -> 1.828 ms per step); with member tiles the
+  // early-resident successors take the slots the other chains' kernels need (config 4:
+  // 1.666 -> 1.769 for all chains, 1.845 for the singleton chains alone; config 2: 0.80 -> 1.02)
+  plan.pdl = std::getenv("HDDM_PDL") ? std::atoi(std::getenv("HDDM_PDL")) : (max_members == 1 ? 1 : 0);
   plan.fwd_leaf = level(leaves);
   plan.bwd_leaf = level(leaves);
   plan.bwd_leafcol = level(leafcols);
@@ -1311,6 +1335,8 @@ CheckArgs hddm_engine::check_args(const cplx* Bp, const cplx* X, const int* zc,
   C.lpq = d_lpq;
   C.nbr = d_nbr;
   C.k2c = d_k2c;
+  C.ctab = d_ctab;
+  C.ctab_off = d_ctab_off;
   C.nsub = nsub;
   C.vm = vmap();
   C.B = Bp;

@@ -57,7 +57,13 @@ struct TileArg {
   const TileRec* rec;
   int ntile;
   int M, E, R;
+  unsigned magM = 0, magE = 0;  // ceil(2^32 / M), ceil(2^32 / E): x / d = umulhi(x, mag) for d > 1
 };
+inline unsigned div_magic(int d) { return d > 1 ? unsigned((0xffffffffull / unsigned(d)) + 1ull) : 0u; }
+inline void tile_mags(TileArg& T) {
+  T.magM = div_magic(T.M);
+  T.magE = div_magic(T.E);
+}
 
 // One level of the level-synchronous sweeps: output items that are independent
 // given the previous levels -- rows (supernode, row) / leaves (leaf, 0) forward,
@@ -119,6 +125,8 @@ struct SolvePlan {
   std::vector<TileRec> tiles;          // host copy of every tile
   std::vector<int> tile_group;         // group of each tile
   bool staged = true;                  // backward pulls through shared memory
+  int pdl = 0;                         // programmatic dependent launch of the level chains:
+                                       // 0 off, 1 every chain, 2 singleton-tile chains only
   // forward: CTA per row above these mean lengths (measured slower at config 4:
   // off by default, HDDM_CTA_RUN / HDDM_CTA_DIAG)
 };
@@ -127,7 +135,6 @@ struct SolvePlan {
 void launch_solve_group(const SolveArgs& A, const SolvePlan& P, int g, cudaStream_t st);
 int solve_launch_count(const SolvePlan& P);  // kernels of one solve over all tiles
 void set_solve_skip(int mask, int only_tile);  // profiling aid (hddm_time_solve only)
-void set_solve_pdl(bool on);                  // programmatic dependent launch of the chains
 // forward lane-shape override of the steady-state plan (tuning): which = 0/1 pulls of
 // singleton / member tiles, 2/3 inverse rows; E = 0 restores the heuristic
 void set_fwd_shape(int which, int level, int E);
@@ -229,6 +236,8 @@ struct CheckArgs {
   const int2* lpq;    // per factor position: window (p, q); p < 0 on the ring
   const int4* nbr;    // per factor position: S, W, E, N neighbour positions (-1: dropped)
   const double* k2c;  // per class: k^2 of its window in factor order
+  const cplx* ctab;          // tabulated row coefficients (k_build_ctab) of the classes with
+  const long long* ctab_off; // ctab_off[c] >= 0 (null: none)
   int nsub;
   VMap vm;
   const cplx* B;
@@ -241,6 +250,7 @@ struct CheckArgs {
   int* refine_flag;  // set when any rel > 1e-11
   double* max_rel;
 };
+void launch_build_ctab(const CheckArgs& A, int c, cplx* tab, cudaStream_t st);
 void launch_check(const CheckArgs& A, cudaStream_t st);           // partials + per-RHS rel
 void launch_check_partials(const CheckArgs& A, cudaStream_t st);  // partials only
 struct RefineArgs;

@@ -280,10 +280,9 @@ constexpr int kCheckUnroll = HDDM_CHECK_UNROLL;
 // from structural tables: window coordinates (lp < 0: ring row)
 // and neighbour positions (S, W, E, N; -1 where the coupling is dropped) per
 // factor-order position, k^2 of the class window in factor order
-template <class XV>
-__device__ __forceinline__ cplx ax_row_t(XV X, int pos, int wnx, int wny, double ih2,
-                                         const cplx* sa, double k2, int2 lpq, int4 nb) {
-  if (lpq.x < 0) return X[pos];
+// coefficients of row (lp, lq): diagonal, S, W, E, N
+__device__ __forceinline__ void row_coefs(int2 lpq, int wnx, int wny, double ih2, const cplx* sa,
+                                          double k2, cplx cf[5]) {
   const int lp = lpq.x, lq = lpq.y;
   const cplx* a1n = sa;
   const cplx* ia1h = sa + wnx;
@@ -293,17 +292,52 @@ __device__ __forceinline__ cplx ax_row_t(XV X, int pos, int wnx, int wny, double
   const cplx ee = cscale(cmul(a2n[lq], ia1h[lp]), ih2);
   const cplx es = cscale(cmul(a1n[lp], ia2h[lq - 1]), ih2);
   const cplx en = cscale(cmul(a1n[lp], ia2h[lq]), ih2);
-  const cplx diag = cadd(cmk(-(ew.x + ee.x + es.x + en.x), -(ew.y + ee.y + es.y + en.y)),
-                         cscale(cmul(a1n[lp], a2n[lq]), k2));
+  cf[0] = cadd(cmk(-(ew.x + ee.x + es.x + en.x), -(ew.y + ee.y + es.y + en.y)),
+               cscale(cmul(a1n[lp], a2n[lq]), k2));
+  cf[1] = es;
+  cf[2] = ew;
+  cf[3] = ee;
+  cf[4] = en;
+}
+
+template <class XV>
+__device__ __forceinline__ cplx ax_apply(XV X, int pos, int4 nb, const cplx cf[5]) {
   const cplx xc = X[pos];
   const cplx xs = nb.x >= 0 ? X[nb.x] : cmk(0, 0), xw = nb.y >= 0 ? X[nb.y] : cmk(0, 0);
   const cplx xe = nb.z >= 0 ? X[nb.z] : cmk(0, 0), xn = nb.w >= 0 ? X[nb.w] : cmk(0, 0);
-  cplx ax = cmul(diag, xc);
-  if (nb.x >= 0) cfma(ax, es, xs);
-  if (nb.y >= 0) cfma(ax, ew, xw);
-  if (nb.z >= 0) cfma(ax, ee, xe);
-  if (nb.w >= 0) cfma(ax, en, xn);
+  cplx ax = cmul(cf[0], xc);
+  if (nb.x >= 0) cfma(ax, cf[1], xs);
+  if (nb.y >= 0) cfma(ax, cf[2], xw);
+  if (nb.z >= 0) cfma(ax, cf[3], xe);
+  if (nb.w >= 0) cfma(ax, cf[4], xn);
   return ax;
+}
+
+template <class XV>
+__device__ __forceinline__ cplx ax_row_t(XV X, int pos, int wnx, int wny, double ih2,
+                                         const cplx* sa, double k2, int2 lpq, int4 nb) {
+  if (lpq.x < 0) return X[pos];
+  cplx cf[5];
+  row_coefs(lpq, wnx, wny, ih2, sa, k2, cf);
+  return ax_apply(X, pos, nb, cf);
+}
+
+// Row coefficients of a class window, tabulated once (classes with several members: every
+// member's check re-reads them as broadcast loads instead of re-forming them from the
+// alpha arrays): tab[pos * 5 + (C, S, W, E, N)]; ring rows (1, 0, 0, 0, 0).
+__global__ void __launch_bounds__(256) k_build_ctab(CheckArgs A, int c, cplx* tab) {
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= A.nw) return;
+  const int2 lq = A.lpq[pos];
+  cplx cf[5] = {cmk(1, 0), cmk(0, 0), cmk(0, 0), cmk(0, 0), cmk(0, 0)};
+  if (lq.x >= 0)
+    row_coefs(lq, A.wnx, A.wny, A.ih2, A.sa + (long long)A.vm.cmem[A.vm.cptr[c]] * A.sa_stride,
+              A.k2c[(long long)c * A.nw + pos], cf);
+  for (int k = 0; k < 5; ++k) tab[(long long)pos * 5 + k] = cf[k];
+}
+
+void launch_build_ctab(const CheckArgs& A, int c, cplx* tab, cudaStream_t st) {
+  k_build_ctab<<<(A.nw + 255) / 256, 256, 0, st>>>(A, c, tab);
 }
 
 // Residual partials of members [k0, k0 + M) of class c over position chunk
@@ -329,6 +363,25 @@ __device__ __forceinline__ void check_block(const CheckArgs& A, int c, int k0, i
     const SVec<const cplx> Bv{A.B + A.vm.cbase[c] + k, m};
     const int chunk = (A.nw + A.nchunk - 1) / A.nchunk;
     const int p0 = blockIdx.x * chunk, p1 = min(A.nw, p0 + chunk);
+    const long long toff = A.ctab_off ? __ldg(A.ctab_off + c) : -1;  // uniform per block
+    if (toff >= 0) {
+      // tabulated coefficients: five broadcast loads per position
+      const cplx* ct = A.ctab + toff;
+      int pos = p0 + pi;
+      int4 nb_n = make_int4(-1, -1, -1, -1);
+      if (pos < p1) nb_n = __ldg(A.nbr + pos);
+      for (; pos < p1; pos += per) {
+        const int4 nb = nb_n;
+        const int pn = pos + per;
+        if (pn < p1) nb_n = __ldg(A.nbr + pn);
+        const cplx b = (A.bmask && !__ldg(A.bmask + pos)) ? cmk(0, 0) : Bv[pos];
+        cplx cf[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) cf[q] = ct[(long long)pos * 5 + q];
+        b2 += cnorm2(b);
+        r2 += cnorm2(csub(b, ax_apply(X, pos, nb, cf)));
+      }
+    } else {
     // the next position's structural tables are loaded one iteration ahead, so
     // the vector / coefficient loads of a position (which depend on them) are
     // the only round trip per iteration
@@ -356,6 +409,7 @@ __device__ __forceinline__ void check_block(const CheckArgs& A, int c, int k0, i
       b2 += cnorm2(b);
       const cplx ax = ax_row_t(X, pos, A.wnx, A.wny, A.ih2, sa, k2, lq, nb);
       r2 += cnorm2(csub(b, ax));
+    }
     }
   }
   sr[tid] = r2;

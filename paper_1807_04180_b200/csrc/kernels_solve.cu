@@ -80,17 +80,26 @@ __device__ __forceinline__ void tile_fill(const SolveArgs& A, const TileArg& T, 
   L.act = in && (A.flag[t] != 0) == (A.flag_on != 0);
 }
 
+// x / d for small x (x * d < 2^32) with mag = ceil(2^32 / d); d == 1: x
+__device__ __forceinline__ unsigned udiv(unsigned x, int d, unsigned mag) {
+  return d == 1 ? x : __umulhi(x, mag);
+}
+
 __device__ __forceinline__ TL tile_lane(const SolveArgs& A, const TileArg& T, int nitem) {
-  const int lane = threadIdx.x & 31;
-  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const long long wpt = (nitem + T.R - 1) / T.R;
-  const int ti = int(w / wpt);
+  // 32-bit unsigned arithmetic and host-side division magics: the lane decomposition
+  // is on every warp's start-up path
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned wpt = (unsigned(nitem) + unsigned(T.R) - 1u) / unsigned(T.R);
+  const unsigned ti = w / wpt;
   TL L;
-  L.k = lane % T.M;
-  L.e = (lane / T.M) % T.E;
-  L.r = lane / (T.M * T.E);
-  L.it = (w - (long long)ti * wpt) * T.R + L.r;
-  tile_fill(A, T, ti, ti < T.ntile && L.r < T.R && L.it < nitem, L);
+  const unsigned q = udiv(lane, T.M, T.magM);   // lane / M
+  const unsigned qe = udiv(q, T.E, T.magE);     // lane / (M E)
+  L.k = int(lane - q * unsigned(T.M));
+  L.e = int(q - qe * unsigned(T.E));
+  L.r = int(qe);
+  L.it = (long long)(w - ti * wpt) * T.R + L.r;
+  tile_fill(A, T, int(ti), int(ti) < T.ntile && L.r < T.R && L.it < nitem, L);
   return L;
 }
 
@@ -119,13 +128,14 @@ __device__ __forceinline__ void csub_mul(cplx& acc, cplx l, cplx x) {
 // U loads of both operands in flight.
 template <int U>
 __device__ __forceinline__ cplx seg_dot(const cplx* __restrict__ vals, const SegRec* __restrict__ sg,
-                                        int ns, int e, int E, const cplx* __restrict__ X, int m) {
+                                        int ns, int e, int E, unsigned magE,
+                                        const cplx* __restrict__ X, int m) {
   cplx acc0 = cmk(0, 0), acc1 = cmk(0, 0);
   const long long xs = (long long)E * m;  // vector stride per step: pointer increments only
   for (int k = 0; k < ns; ++k) {
     const SegRec r = sg[k];
     if (e >= r.len) continue;
-    int n = (r.len - 1 - e) / E + 1;  // entries of this lane
+    int n = int(udiv(unsigned(r.len - 1 - e), E, magE)) + 1;  // entries of this lane
     const cplx* lp = vals + r.off + e;
     const cplx* xp = X + (long long)(r.zb + e) * m;
     for (; n >= U; n -= U) {  // full batches of U
@@ -288,7 +298,7 @@ __global__ void __launch_bounds__(kThreads) k_fwd_pull(SolveArgs A, TileArg T, c
   cplx acc = cmk(0, 0);
   if (live) {
     R = __ldg(rec + it);
-    acc = seg_dot<kUF>(A.vals + (long long)L.c * A.nvals, A.fseg + R.y, R.z, L.e, T.E, A.X + L.cb,
+    acc = seg_dot<kUF>(A.vals + (long long)L.c * A.nvals, A.fseg + R.y, R.z, L.e, T.E, T.magE, A.X + L.cb,
                        L.m);
   }
   if (T.E > 1) acc = tile_reduce(acc, T, L);
@@ -677,9 +687,9 @@ __global__ void __launch_bounds__(kSplitWarps * 32) k_bwd_split(SolveArgs A, Til
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ti = blockIdx.x / nitem;  // CTA per (tile, column group)
   TL L;
-  L.k = lane % T.M;
+  L.r = int(udiv(unsigned(lane), T.M, T.magM));
+  L.k = lane - L.r * T.M;
   L.e = 0;
-  L.r = lane / T.M;
   L.it = 0;
   tile_fill(A, T, ti, L.r < T.R, L);
   const int2 item = items[blockIdx.x - ti * nitem];
@@ -976,7 +986,7 @@ int solve_launch_count(const SolvePlan& P) {
   return int(P.groups.size()) * (4 + 2 * int(P.fwd.size()) + 2 * int(P.bwd.size()));
 }
 
-static bool g_pdl = false;
+static bool g_pdl = false;   // the chain being enqueued (SolvePlan::pdl)
 
 // launch with programmatic stream serialization (see pdl_trigger / pdl_wait)
 template <typename... KArgs, typename... Args>
@@ -995,8 +1005,6 @@ static void launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, size_
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, k, args...);
 }
-
-void set_solve_pdl(bool on) { g_pdl = on; }
 
 static unsigned blocks_for(long long threads) {
   return unsigned((threads + kThreads - 1) / kThreads);
@@ -1067,6 +1075,7 @@ static int fwd_shape(int M, long avg, bool diag, bool sparse, int level) {
 static TileArg with_shape(TileArg T, int E) {
   T.E = E;
   T.R = std::max(1, 32 / (E * T.M));
+  tile_mags(T);
   return T;
 }
 
@@ -1100,6 +1109,7 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
   if (g_only >= 0 && g != g_only) return;
   if (g_only <= -2 && P.groups[g].M != -2 - g_only) return;  // HDDM_ONLY_M (time_solve only)
   const TileArg T1 = with_shape(P.groups[g], 1);  // thread per (item, member)
+  g_pdl = P.pdl == 1 || (P.pdl == 2 && P.groups[g].M == 1);
   // substitution for the mid-size separators: tiles of at least this many members
   static const int subst_min_m = std::getenv("HDDM_SUBST_MIN_M") ? std::atoi(std::getenv("HDDM_SUBST_MIN_M")) : 2;
   const long long nt = T1.ntile;

@@ -29,9 +29,9 @@ def line_map(lib, func_sub):
         cur = None
         out = {}
         for ln in m.splitlines():
-            g = re.search(r'line (\d+)', ln) if "//## File" in ln else None
+            g = re.search(r'File "([^"]+)", line (\d+)', ln) if "//## File" in ln else None
             if g:
-                cur = int(g.group(1))
+                cur = (g.group(1), int(g.group(2)))
                 continue
             a = re.search(r'/\*([0-9a-f]{4,})\*/', ln)
             if a and cur is not None:
@@ -53,24 +53,31 @@ def samples(rep, kregex):
             hdr = {k: i for i, k in enumerate(r)}
             continue
         if hdr and len(r) >= len(hdr):
-            out.append((int(r[hdr["Address"]], 16), float(r[hdr["Warp Stall Sampling (All Samples)"]] or 0)))
-    base = min(a for a, _ in out)
-    return [(a - base, s) for a, s in out]
+            out.append((int(r[hdr["Address"]], 16), float(r[hdr["Warp Stall Sampling (All Samples)"]] or 0),
+                        float(r[hdr["Instructions Executed"]] or 0)))
+    base = min(a for a, _, _ in out)
+    return [(a - base, s, n) for a, s, n in out]
 
 
 def main():
     rep, kre, lib, fsub = sys.argv[1:5]
     top = int(sys.argv[5]) if len(sys.argv) > 5 else 25
     lm = line_map(lib, fsub)
-    src = open(os.path.join(os.path.dirname(lib), "csrc", "kernels_solve.cu")).read().splitlines() \
-        if os.path.exists(os.path.join(os.path.dirname(lib), "csrc", "kernels_solve.cu")) else []
+    files = {}
     acc = collections.Counter()
-    for off, s in samples(rep, kre):
-        acc[lm.get(off, -1)] += s
+    ins = collections.Counter()
+    for off, s, n in samples(rep, kre):
+        acc[lm.get(off, ("?", 0))] += s
+        ins[lm.get(off, ("?", 0))] += n
     tot = sum(acc.values())
-    for ln, s in acc.most_common(top):
+    itot = sum(ins.values()) or 1
+    print(f"warp instructions executed: {itot:.0f}")
+    for (fn, ln), s in acc.most_common(top):
+        if fn not in files:
+            files[fn] = open(fn).read().splitlines() if os.path.exists(fn) else []
+        src = files[fn]
         text = src[ln - 1].strip()[:90] if 0 < ln <= len(src) else ""
-        print(f"{100 * s / tot:5.1f}%  L{ln:<5d} {text}")
+        print(f"{100 * s / tot:5.1f}% stall {100 * ins[(fn, ln)] / itot:5.1f}% inst  {os.path.basename(fn)}:{ln:<5d} {text}")
 
 
 if __name__ == "__main__":

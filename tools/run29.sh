@@ -1,0 +1,11 @@
+#!/bin/bash
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+for cfg in 4 2 3 1; do
+PCFG=$cfg TAG="cfg$cfg" python tools/time_step.py 2>&1 | grep RESULT
+HDDM_CTAB_MIN=100000 PCFG=$cfg TAG="cfg$cfg noctab" python tools/time_step.py 2>&1 | grep RESULT
+done
+TAG=cfg4 python tools/stage_prof.py 2>&1 | grep STAGE
+PCFG=4 python tools/solve_once.py 2>&1 | tail -1
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_ref_live.py tests/test_gpu_properties.py tests/test_gpu_shard.py -m gpu -q -x > gpurun_out/s5_parity.log 2>&1
+echo "pytest rc=$?"; tail -n 3 gpurun_out/s5_parity.log
