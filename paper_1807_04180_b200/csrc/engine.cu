@@ -90,6 +90,8 @@ struct hddm_engine {
   int* d_bw_ptr = nullptr;
   std::vector<int> h_bw_ptr;
   BwRow* d_bw = nullptr;
+  int* d_bw_cnt = nullptr;       // per factor position: backward rows reaching the column
+  std::vector<int> h_bw_cnt;
   int* d_perm = nullptr;
   int* d_pinv = nullptr;
   SolvePlan plan;
@@ -449,6 +451,16 @@ void hddm_engine::create(const hddm_problem& p) {
     d_bw_ptr = upload(bptr);
     h_bw_ptr = bptr;
     d_bw = upload(bw);
+    // rows reaching each column (first <= column): a prefix of the sorted list
+    h_bw_cnt.assign(Y.n, 0);
+    for (size_t s = 0; s < Y.sn.size(); ++s) {
+      int k = bptr[s];
+      for (int j = 0; j < Y.sn[s].n; ++j) {
+        while (k < bptr[s + 1] && bw[k].first <= j) ++k;
+        h_bw_cnt[Y.sn[s].c0 + j] = k - bptr[s];
+      }
+    }
+    d_bw_cnt = upload(h_bw_cnt);
   }
 
   // ---- per-subdomain data
@@ -840,7 +852,7 @@ void hddm_engine::build_plan() {
     for (int s : sns)
       for (int j = 0; j < Y.sn[s].n; j += stage_cw) {
         const int j1 = std::min(Y.sn[s].n, j + stage_cw);
-        ch.push_back(make_int4(s, j, j1, 0));
+        ch.push_back(make_int4(s, j, j1, h_bw_cnt[Y.sn[s].c0 + j1 - 1]));
         cw = std::max(cw, j1 - j);
       }
     L.nchunk4 = int(ch.size());
@@ -1181,6 +1193,7 @@ SolveArgs hddm_engine::solve_args(const cplx* Bp, cplx* X, cplx* Yp, const int* 
   A.seg = d_seg;
   A.bw_ptr = d_bw_ptr;
   A.bw = d_bw;
+  A.bw_cnt = d_bw_cnt;
   A.vals = d_vals;
   A.nvals = Y.nvals;
   A.lss = d_lss;

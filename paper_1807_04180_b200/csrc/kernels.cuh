@@ -23,6 +23,8 @@ struct SolveArgs {
   const int2* seg;           // (length, first source position)
   const int* bw_ptr;         // per supernode: backward rows
   const BwRow* bw;
+  const int* bw_cnt;         // per factor position (column): its supernode's backward rows that
+                             // reach it (rows with first <= column; the lists are sorted by first)
   const SegRec* fseg;  // forward run segments of the plan in use (full or sparse RHS)
   const cplx* vals;    // ncls x nvals
   long long nvals;

@@ -85,6 +85,14 @@ __device__ __forceinline__ unsigned udiv(unsigned x, int d, unsigned mag) {
   return d == 1 ? x : __umulhi(x, mag);
 }
 
+// the same, opaque to the optimiser: recomputed where it is used instead of being hoisted
+// out of a loop into registers (k_bwd_stage's pair indices: 80 -> 126 registers if hoisted)
+__device__ __forceinline__ unsigned udiv_here(unsigned x, int d, unsigned mag) {
+  unsigned q;
+  asm volatile("mul.hi.u32 %0, %1, %2;" : "=r"(q) : "r"(x), "r"(mag));
+  return d == 1 ? x : q;
+}
+
 __device__ __forceinline__ TL tile_lane(const SolveArgs& A, const TileArg& T, int nitem) {
   // 32-bit unsigned arithmetic and host-side division magics: the lane decomposition
   // is on every warp's start-up path
@@ -170,16 +178,6 @@ __device__ __forceinline__ cplx seg_dot(const cplx* __restrict__ vals, const Seg
 // forward skipped hold z = 0 exactly and X is not cleared for them
 __device__ __forceinline__ cplx zval(const SolveArgs& A, int s, long long p) {
   return (A.sn_live != nullptr && A.sn_live[s] == 0) ? cmk(0, 0) : A.X[p];
-}
-
-// rows of a backward list (sorted by first stored column) that touch column j
-__device__ __forceinline__ int rows_upto(const BwRow* rows, int nr, int j) {
-  int lo = 0, hi = nr;  // first index with first > j
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (rows[mid].first <= j) lo = mid + 1; else hi = mid;
-  }
-  return lo;
 }
 
 // sum over rows k = start, start+step, ... < nr of L[r][j] * X[dpos_r * m],
@@ -559,7 +557,7 @@ __global__ void __launch_bounds__(256) k_bwd_mma(SolveArgs A, TileArg T, const i
     }
   } else {
     const BwRow* rows = A.bw + A.bw_ptr[it0.x];
-    const int nr = rows_upto(rows, A.bw_ptr[it0.x + 1] - A.bw_ptr[it0.x], j0 + B.y - 1);
+    const int nr = __ldg(A.bw_cnt + sn.c0 + j0 + B.y - 1);
     const cplx* Xb = A.X + cb;
     for (int r0 = 4 * wp; r0 < nr; r0 += 32) {
       const int rk = r0 + q;
@@ -626,7 +624,7 @@ __global__ void __launch_bounds__(kThreads) k_bwd_pull(SolveArgs A, TileArg T, c
   const int j = item.y;
   const cplx* vals = A.vals + (long long)L.c * A.nvals;
   const BwRow* rows = A.bw + A.bw_ptr[item.x];
-  const int nr = rows_upto(rows, A.bw_ptr[item.x + 1] - A.bw_ptr[item.x], j);
+  const int nr = __ldg(A.bw_cnt + sn.c0 + j);
   const cplx acc = bw_gather<kUB>(vals, rows, 0, nr, 1, j, A.X + L.cb, L.m);
   const long long p = vat(L, sn.c0 + j);
   (TO_X ? A.X : A.Y)[p] = csub(cmul(ldg(vals + sn.dinv_off + j), zval(A, item.x, p)), acc);
@@ -707,7 +705,7 @@ __global__ void __launch_bounds__(kSplitWarps * 32) k_bwd_split(SolveArgs A, Til
         cfma(acc, ldf(Linv + (long long)i * (i - 1) / 2 + j), y[i]);
     } else {
       const BwRow* rows = A.bw + A.bw_ptr[item.x];
-      const int nr = rows_upto(rows, A.bw_ptr[item.x + 1] - A.bw_ptr[item.x], j);
+      const int nr = __ldg(A.bw_cnt + sn.c0 + j);
       acc = bw_gather<kUB>(vals, rows, warp, nr, kSplitWarps, j, A.X + L.cb, L.m);
     }
   }
@@ -748,7 +746,7 @@ __global__ void __launch_bounds__(kStageThreads) k_bwd_stage(SolveArgs A, TileAr
   extern __shared__ __align__(16) unsigned char smem[];
   pdl_trigger();
   const int ti = blockIdx.x / nchunk;
-  const int4 ch = chunks[blockIdx.x - ti * nchunk];  // (supernode, j0, j1, -)
+  const int4 ch = chunks[blockIdx.x - ti * nchunk];  // (supernode, j0, j1, rows reaching j1 - 1)
   const TileRec* rec = T.rec + ti;
   const int M = T.M, m = rec->m;
   const long long cb = rec->cb;
@@ -760,23 +758,28 @@ __global__ void __launch_bounds__(kStageThreads) k_bwd_stage(SolveArgs A, TileAr
   const DevSn sn = A.sn[ch.x];
   const int j0 = ch.y, CW = ch.z - ch.y;
   const BwRow* rows = A.bw + A.bw_ptr[ch.x];
-  const int nre = rows_upto(rows, A.bw_ptr[ch.x + 1] - A.bw_ptr[ch.x], ch.z - 1);
+  const int nre = ch.w;  // rows reaching the chunk's last column (a prefix of the sorted list)
   const cplx* vals = A.vals + (long long)rec->c * A.nvals;
   cplx* xs = reinterpret_cast<cplx*>(smem);            // [RC][M]
   cplx* ls = xs + (size_t)RC * M;                        // [RC][CW]
   BwRow* rd = reinterpret_cast<BwRow*>(ls + (size_t)RC * CWmax);  // [RC]
   cplx* red = reinterpret_cast<cplx*>(rd + RC);          // [kStageThreads] split partials
   const int P = CW * M;                                  // (column, member) pairs
-  const int S = P >= kStageThreads ? 1 : kStageThreads / P;  // row splits
-  const int pp = tid % P, sp = tid / P;  // split mode: pair, row split
+  // small quotients through a float reciprocal: n / d = int((n + 0.5f) * (1 / d)), exact for
+  // n, d <= 1024 (the distance to the next integer is >= 0.5 / d, the error < 2e-5)
+  const float rP = __frcp_rn(float(P));
+  const int S = P >= kStageThreads ? 1 : int((kStageThreads + 0.5f) * rP);  // row splits
+  const int sp = int((tid + 0.5f) * rP), pp = tid - sp * P;  // split mode: row split, pair
   constexpr int kMaxQ = 1024 / kStageThreads;  // pairs per thread (P <= 32 x 32)
   cplx acc[kMaxQ];
 #pragma unroll
   for (int q = 0; q < kMaxQ; ++q) acc[q] = cmk(0, 0);
   pdl_wait();
   // staging lanes on (row, member) and (row, column) grids: no divisions in the loops
-  const int xr = tid / M, xm = tid - xr * M, xrows = kStageThreads / M;
-  const int lr = tid / CW, lc = tid - lr * CW, lrows = kStageThreads / CW;
+  const int xr = int(udiv(unsigned(tid), M, T.magM)), xm = tid - xr * M;
+  const int xrows = int(udiv(unsigned(kStageThreads), M, T.magM));
+  const float rCW = __frcp_rn(float(CW));
+  const int lr = int((tid + 0.5f) * rCW), lc = tid - lr * CW, lrows = int((kStageThreads + 0.5f) * rCW);
   const cplx* Xb = A.X + cb + xm;
   for (int k0 = 0; k0 < nre; k0 += RC) {
     const int kc = min(RC, nre - k0);
@@ -801,7 +804,7 @@ __global__ void __launch_bounds__(kStageThreads) k_bwd_stage(SolveArgs A, TileAr
       for (int q = 0; q < kMaxQ; ++q) {
         const int p = tid + q * kStageThreads;
         if (p < P) {
-          const int jj = p / M, mm = p - jj * M;
+          const int jj = int(udiv_here(unsigned(p), M, T.magM)), mm = p - jj * M;
           cplx a = acc[q], a2 = cmk(0, 0);
           int kk = 0;
           for (; kk + 1 < kc; kk += 2) {
@@ -833,7 +836,7 @@ __global__ void __launch_bounds__(kStageThreads) k_bwd_stage(SolveArgs A, TileAr
   for (int q = 0; q < kMaxQ; ++q) {
     const int p = tid + q * kStageThreads;
     if (p < P && (S == 1 || q == 0)) {
-      const int jj = p / M, mm = p - jj * M;
+      const int jj = int(udiv_here(unsigned(p), M, T.magM)), mm = p - jj * M;
       if ((A.flag[rec->t[mm]] != 0) == (A.flag_on != 0)) {
         const int j = j0 + jj;
         const long long a = cb + (long long)(sn.c0 + j) * m + mm;

@@ -46,17 +46,20 @@ def samples(rep, kregex):
     rows = list(csv.reader(txt.splitlines()))
     hdr = None
     out = []
+    done = []
     for r in rows:
-        if r and r[0] == "Address":
-            if hdr is not None:
-                break  # first kernel only
+        if r and r[0] == "Address":  # one table per launch: all matching launches are summed
             hdr = {k: i for i, k in enumerate(r)}
+            if out:
+                base0 = min(a for a, _, _ in out)
+                done.extend((a - base0, s_, n) for a, s_, n in out)
+                out = []
             continue
         if hdr and len(r) >= len(hdr):
             out.append((int(r[hdr["Address"]], 16), float(r[hdr["Warp Stall Sampling (All Samples)"]] or 0),
                         float(r[hdr["Instructions Executed"]] or 0)))
     base = min(a for a, _, _ in out)
-    return [(a - base, s, n) for a, s, n in out]
+    return done + [(a - base, s, n) for a, s, n in out]
 
 
 def main():
