@@ -134,14 +134,18 @@ __device__ __forceinline__ void csub_mul(cplx& acc, cplx l, cplx x) {
 // contiguous piece of the factor values against consecutive source positions,
 // so no per-element index is loaded; lanes e, e+E, ... stride each segment with
 // U loads of both operands in flight.
-template <int U>
+template <int U, bool PF>
 __device__ __forceinline__ cplx seg_dot(const cplx* __restrict__ vals, const SegRec* __restrict__ sg,
                                         int ns, int e, int E, unsigned magE,
                                         const cplx* __restrict__ X, int m) {
   cplx acc0 = cmk(0, 0), acc1 = cmk(0, 0);
   const long long xs = (long long)E * m;  // vector stride per step: pointer increments only
+  // PF (singleton tiles): the next segment's record is loaded behind this one's data, one
+  // dependent round trip less per segment; member tiles keep the registers (measured)
+  SegRec rn = (PF && ns > 0) ? sg[0] : SegRec{0, 0, 0};
   for (int k = 0; k < ns; ++k) {
-    const SegRec r = sg[k];
+    const SegRec r = PF ? rn : sg[k];
+    if (PF && k + 1 < ns) rn = sg[k + 1];
     if (e >= r.len) continue;
     int n = int(udiv(unsigned(r.len - 1 - e), E, magE)) + 1;  // entries of this lane
     const cplx* lp = vals + r.off + e;
@@ -285,6 +289,7 @@ __global__ void __launch_bounds__(kThreads) k_fwd_leaf(SolveArgs A, TileArg T, c
 
 // separator rows, forward pull: Y[r] = B[r] - run(r) . X[src].
 // rec[item] = (position, first segment in A.fseg, segment count, -).
+template <bool PF>
 __global__ void __launch_bounds__(kThreads) k_fwd_pull(SolveArgs A, TileArg T, const int4* rec,
                                                        int nitem) {
   pdl_trigger();
@@ -296,7 +301,7 @@ __global__ void __launch_bounds__(kThreads) k_fwd_pull(SolveArgs A, TileArg T, c
   cplx acc = cmk(0, 0);
   if (live) {
     R = __ldg(rec + it);
-    acc = seg_dot<kUF>(A.vals + (long long)L.c * A.nvals, A.fseg + R.y, R.z, L.e, T.E, T.magE, A.X + L.cb,
+    acc = seg_dot<kUF, PF>(A.vals + (long long)L.c * A.nvals, A.fseg + R.y, R.z, L.e, T.E, T.magE, A.X + L.cb,
                        L.m);
   }
   if (T.E > 1) acc = tile_reduce(acc, T, L);
@@ -1136,7 +1141,7 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
     if (TS.ntile > 0 && L.avg_run > P.sub_run) {  // long rows: sub-tiles
       const TileArg Tp = with_shape(TS, fwd_lanes(TS.M, L.avg_run));
       if (!(skip & 4))
-        launch_pdl(k_fwd_pull, blocks_n(Tp.ntile, L.nitem, Tp.R), kThreads, 0, st, A, Tp,
+        launch_pdl(Tp.M == 1 ? k_fwd_pull<true> : k_fwd_pull<false>, blocks_n(Tp.ntile, L.nitem, Tp.R), kThreads, 0, st, A, Tp,
                    (const int4*)L.d_rec, L.nitem);
       const TileArg Td = with_shape(TS, fwd_lanes(TS.M, L.avg_diag, true));
       if (!(skip & 8))
@@ -1162,7 +1167,7 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
                    (const MmaSeg*)L.d_mseg, L.nmblk);
     } else {
       const TileArg Tp = with_shape(T1, fwd_shape(T1.M, L.avg_run, false, sp, li));
-      launch_pdl(k_fwd_pull, blocks(L.nitem, Tp.R), kThreads, 0, st, A, Tp, (const int4*)L.d_rec,
+      launch_pdl(Tp.M == 1 ? k_fwd_pull<true> : k_fwd_pull<false>, blocks(L.nitem, Tp.R), kThreads, 0, st, A, Tp, (const int4*)L.d_rec,
                  L.nitem);
     }
     if (skip & 8) {
