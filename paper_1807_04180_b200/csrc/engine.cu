@@ -351,7 +351,7 @@ struct hddm_engine {
     }
     return mask;
   }
-  int solve_launches() const { return solve_launch_count(plan); }
+  int solve_launches() { return solve_launch_count(plan, solve_args(d_B, d_U[0], d_Y, d_zero, 0)); }
 };
 
 // ----------------------------------------------------------------- creation
@@ -849,6 +849,8 @@ void hddm_engine::build_plan() {
   auto chunks4 = [&](SolveLevel& L, const std::vector<int>& sns) {
     std::vector<int4> ch;
     int cw = 0;
+    L.one_chunk = !sns.empty();
+    for (int s : sns) L.one_chunk = L.one_chunk && Y.sn[s].n <= stage_cw;
     for (int s : sns)
       for (int j = 0; j < Y.sn[s].n; j += stage_cw) {
         const int j1 = std::min(Y.sn[s].n, j + stage_cw);
@@ -2303,7 +2305,7 @@ int hddm_time_solve(hddm_engine* e, int reps, double* ms_per_solve) {
   });
 }
 
-int hddm_solve_launches(const hddm_engine* e) { return solve_launch_count(e->plan); }
+int hddm_solve_launches(const hddm_engine* e) { return const_cast<hddm_engine*>(e)->solve_launches(); }
 
 int hddm_time_kernel(hddm_engine* e, int which, int reps, double* ms_per_launch) {
   return guarded(e, [&] {

@@ -100,6 +100,7 @@ struct SolveLevel {
   int nchunk4 = 0;
   int4* d_chunks4 = nullptr;
   int cw_max = 0;
+  bool one_chunk = false;   // every supernode of the level is one chunk (n <= the chunk width)
   // the level's separators (supernode, 0) for the substitution kernels
   int nsep = 0, nmax_sep = 0;
   int2* d_seps = nullptr;
@@ -135,7 +136,7 @@ struct SolvePlan {
 
 // one tile group's full solve (all levels) on one stream
 void launch_solve_group(const SolveArgs& A, const SolvePlan& P, int g, cudaStream_t st);
-int solve_launch_count(const SolvePlan& P);  // kernels of one solve over all tiles
+int solve_launch_count(const SolvePlan& P, const SolveArgs& A);  // kernels of one solve over all tiles
 void set_solve_skip(int mask, int only_tile);  // profiling aid (hddm_time_solve only)
 // forward lane-shape override of the steady-state plan (tuning): which = 0/1 pulls of
 // singleton / member tiles, 2/3 inverse rows; E = 0 restores the heuristic

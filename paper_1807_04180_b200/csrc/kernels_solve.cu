@@ -744,7 +744,10 @@ __global__ void __launch_bounds__(kSplitWarps * 32) k_bwd_split(SolveArgs A, Til
 #endif
 constexpr int kStageThreads = HDDM_STAGE_THREADS;
 
-template <bool TO_X>
+// MODE 0: w -> Y (a diagonal kernel follows); 1: leaf columns, w -> X; 2: every chunk is a
+// whole separator (n <= 32 columns): w stays in shared memory and the dense-inverse product
+// x_j = w_j + sum_{i>j} Linv[i][j] w_i follows in the same CTA (one kernel less per level)
+template <int MODE>
 __global__ void __launch_bounds__(kStageThreads) k_bwd_stage(SolveArgs A, TileArg T,
                                                              const int4* chunks, int nchunk,
                                                              int RC, int CWmax) {
@@ -837,6 +840,43 @@ __global__ void __launch_bounds__(kStageThreads) k_bwd_stage(SolveArgs A, TileAr
       acc[0] = a;
     }
   }
+  if (MODE == 2) {
+    cplx* ws = xs;  // [CW][M]: the pulled w of the whole separator (the staging loop ended on a barrier)
+#pragma unroll
+    for (int q = 0; q < kMaxQ; ++q) {
+      const int p = tid + q * kStageThreads;
+      if (p < P && (S == 1 || q == 0)) {
+        const int jj = int(udiv_here(unsigned(p), M, T.magM)), mm = p - jj * M;
+        const long long a = cb + (long long)(sn.c0 + jj) * m + mm;
+        ws[p] = csub(cmul(ldg(vals + sn.dinv_off + jj), zval(A, ch.x, a)), acc[q]);
+      }
+    }
+    __syncthreads();
+    const cplx* Linv = vals + sn.diag_off;
+#pragma unroll
+    for (int q = 0; q < kMaxQ; ++q) {
+      const int p = tid + q * kStageThreads;
+      if (p < P && (S == 1 || q == 0)) {
+        const int jj = int(udiv_here(unsigned(p), M, T.magM)), mm = p - jj * M;
+        if ((A.flag[rec->t[mm]] != 0) == (A.flag_on != 0)) {
+          cplx x = ws[p], x2 = cmk(0, 0);
+          int i = jj + 1;
+          const cplx* lp = Linv + (long long)i * (i - 1) / 2 + jj;  // column jj of the packed inverse
+          const cplx* wp = ws + i * M + mm;
+          for (; i + 2 <= CW; i += 2) {
+            const cplx l0 = ldf(lp), l1 = ldf(lp + i);
+            cfma(x, l0, wp[0]);
+            cfma(x2, l1, wp[M]);
+            lp += 2 * i + 1;
+            wp += 2 * M;
+          }
+          if (i < CW) cfma(x, ldf(lp), wp[0]);
+          A.X[cb + (long long)(sn.c0 + jj) * m + mm] = cadd(x, x2);
+        }
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int q = 0; q < kMaxQ; ++q) {
     const int p = tid + q * kStageThreads;
@@ -845,7 +885,7 @@ __global__ void __launch_bounds__(kStageThreads) k_bwd_stage(SolveArgs A, TileAr
       if ((A.flag[rec->t[mm]] != 0) == (A.flag_on != 0)) {
         const int j = j0 + jj;
         const long long a = cb + (long long)(sn.c0 + j) * m + mm;
-        (TO_X ? A.X : A.Y)[a] = csub(cmul(ldg(vals + sn.dinv_off + j), zval(A, ch.x, a)), acc[q]);
+        (MODE == 1 ? A.X : A.Y)[a] = csub(cmul(ldg(vals + sn.dinv_off + j), zval(A, ch.x, a)), acc[q]);
       }
     }
   }
@@ -977,6 +1017,9 @@ __global__ void __launch_bounds__(512) k_sep_trsv(SolveArgs A, TileArg T, const 
   }
 }
 
+static bool g_dry = false;  // count the launches of a solve without launching (solve_launch_count)
+static int g_count = 0;
+
 template <bool BWD>
 static void launch_sep_trsv(const SolveArgs& A, const TileArg& T, const SolveLevel& L, cudaStream_t st) {
   const size_t smem = size_t(L.nmax_sep) * (L.nmax_sep - 1) / 2 * sizeof(cplx);
@@ -986,14 +1029,12 @@ static void launch_sep_trsv(const SolveArgs& A, const TileArg& T, const SolveLev
     cudaFuncSetAttribute(k_sep_trsv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     attr = true;
   }
+  ++g_count;
+  if (g_dry) return;
   k_sep_trsv<BWD><<<unsigned(T.ntile * L.nsep), 32 * T.M, smem, st>>>(A, T, (const int2*)L.d_seps, L.nsep);
 }
 
 // ------------------------------------------------------------------ launcher
-int solve_launch_count(const SolvePlan& P) {
-  return int(P.groups.size()) * (4 + 2 * int(P.fwd.size()) + 2 * int(P.bwd.size()));
-}
-
 static bool g_pdl = false;   // the chain being enqueued (SolvePlan::pdl)
 
 // launch with programmatic stream serialization (see pdl_trigger / pdl_wait)
@@ -1001,6 +1042,8 @@ template <typename... KArgs, typename... Args>
 static void launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem,
                        cudaStream_t st, Args... args) {
   if (grid == 0) return;
+  ++g_count;
+  if (g_dry) return;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
@@ -1100,14 +1143,14 @@ void set_solve_skip(int mask, int only_tile) {
 }
 
 // staged backward pull over a level's column chunks
-template <bool TO_X>
+template <int MODE>
 static void launch_bwd_stage(const SolveArgs& A, const TileArg& T, const SolveLevel& L,
                              cudaStream_t st) {
   constexpr int kBudget = HDDM_STAGE_KB * 1024;  // staging buffer per CTA
   const int rowb = (T.M + L.cw_max + 1) * int(sizeof(cplx));
   const int RC = std::max(1, (kBudget - kStageThreads * int(sizeof(cplx))) / rowb);
   const size_t smem = size_t(RC) * rowb + kStageThreads * sizeof(cplx);
-  launch_pdl(k_bwd_stage<TO_X>, unsigned((long long)T.ntile * L.nchunk4), kStageThreads, smem, st,
+  launch_pdl(k_bwd_stage<MODE>, unsigned((long long)T.ntile * L.nchunk4), kStageThreads, smem, st,
              A, T, (const int4*)L.d_chunks4, L.nchunk4, RC, L.cw_max);
 }
 
@@ -1127,7 +1170,10 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
   SolveArgs A = A0;
   A.fseg = sp ? P.d_fseg_sp : P.d_fseg;
   A.sn_live = sp ? P.d_sn_live : nullptr;
-  if (!(skip & 1)) k_ring<<<blocks(A.nring, T1.R), kThreads, 0, st>>>(A, T1);
+  if (!(skip & 1)) {
+    ++g_count;
+    if (!g_dry) k_ring<<<blocks(A.nring, T1.R), kThreads, 0, st>>>(A, T1);
+  }
   const SolveLevel& FL = sp ? P.fwd_leaf_sp : P.fwd_leaf;
   if (!(skip & 2) && FL.nitem > 0)
     launch_pdl(k_fwd_leaf, blocks(FL.nitem, T1.R), kThreads, 0, st, A, T1, (const int2*)FL.d_items,
@@ -1203,22 +1249,31 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
     // the pulls stay on the staged kernel (measured: the tensor-core pull 1.699 -> 1.731 ms
     // per config-4 step); HDDM_MMA_BPULL=1 selects it
     static const bool mma_bpull = std::getenv("HDDM_MMA_BPULL") && std::getenv("HDDM_MMA_BPULL")[0] == '1';
+    static const long mma_bdiag_min =
+        std::getenv("HDDM_MMA_DIAG_MIN") ? std::atol(std::getenv("HDDM_MMA_DIAG_MIN")) : 32;
+    // small separators (one staged chunk each, dense inverse): pull and inverse product in
+    // one kernel (HDDM_FUSE_BWD=0: two kernels)
+    static const bool fuse_bwd = !(std::getenv("HDDM_FUSE_BWD") && std::getenv("HDDM_FUSE_BWD")[0] == '0');
+    const bool trsv = A.lss && L.nsep > 0 && T1.M >= subst_min_m && T1.M <= 16;
+    const bool fuse = fuse_bwd && staged && !use_sub && L.one_chunk && !trsv && !(skip & 48) &&
+                      !(mma_ok && (mma_bpull || L.avg_diag >= mma_bdiag_min));
     if (skip & 16) {
     } else if (mma_ok && mma_bpull) {
       if (T1.M <= 8)
         launch_pdl(k_bwd_mma<1, false>, gm, 256, 0, st, A, T1, (const int2*)L.d_items, (const int4*)L.d_mblk, L.nmblk);
       else
         launch_pdl(k_bwd_mma<2, false>, gm, 256, 0, st, A, T1, (const int2*)L.d_items, (const int4*)L.d_mblk, L.nmblk);
+    } else if (fuse) {
+      launch_bwd_stage<2>(A, T1, L, st);
+      continue;
     } else if (staged)
-      launch_bwd_stage<false>(A, use_sub ? with_shape(TS, 1) : T1, L, st);
+      launch_bwd_stage<0>(A, use_sub ? with_shape(TS, 1) : T1, L, st);
     else if (L.split_rows && has_grp)
       launch_pdl(k_bwd_split<false>, gs, kSplitWarps * 32, 0, st, A, T1, (const int2*)grp->second.second,
                  grp->second.first);
     else
       launch_pdl(k_bwd_pull<false>, blocks(L.nitem, T1.R), kThreads, 0, st, A, T1,
                  (const int2*)L.d_items, L.nitem);
-    static const long mma_bdiag_min =
-        std::getenv("HDDM_MMA_DIAG_MIN") ? std::atol(std::getenv("HDDM_MMA_DIAG_MIN")) : 32;
     if (skip & 32) {
     } else if (A.lss && L.nsep > 0 && T1.M >= subst_min_m && T1.M <= 16) {
       launch_sep_trsv<true>(A, T1, L, st);
@@ -1239,7 +1294,7 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
     static const int leaf_min_m =
         std::getenv("HDDM_LEAF_STAGE_MIN_M") ? std::atoi(std::getenv("HDDM_LEAF_STAGE_MIN_M")) : 2;
     if (P.staged && T1.M >= leaf_min_m)
-      launch_bwd_stage<true>(A, T1, BC, st);
+      launch_bwd_stage<1>(A, T1, BC, st);
     else
       launch_pdl(k_bwd_pull<true>, blocks(BC.nitem, T1.R), kThreads, 0, st, A, T1,
                  (const int2*)BC.d_items, BC.nitem);
@@ -1248,6 +1303,15 @@ void launch_solve_group(const SolveArgs& A0, const SolvePlan& P, int g, cudaStre
   if (!(skip & 128))
     launch_pdl(k_bwd_leaf, blocks(BL.nitem, T1.R), kThreads, 0, st, A, T1, (const int2*)BL.d_items,
                BL.nitem);
+}
+
+// kernels of one solve over all tile groups: a dry run of the launch logic
+int solve_launch_count(const SolvePlan& P, const SolveArgs& A) {
+  g_dry = true;
+  g_count = 0;
+  for (int g = 0; g < int(P.groups.size()); ++g) launch_solve_group(A, P, g, nullptr);
+  g_dry = false;
+  return g_count;
 }
 
 }  // namespace hddm
