@@ -335,6 +335,23 @@ __global__ void __launch_bounds__(256) k_fwd_pull_mma(SolveArgs A, TileArg T, co
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int ti = blockIdx.x / nblk;
   const int b = blockIdx.x - ti * nblk;
+  // static tables first (written at setup): the block record and its first segment are in
+  // flight while the activity flags resolve
+  const int4 B = blk[b];  // (first item, rows, first segment, segments)
+  const int g = lane >> 2, q = lane & 3;
+  const bool grow = g < B.y;
+  int zmin_n = 0, ulen_n = 0, lo_n = 0, hi_n = 0;
+  long long vb_n = 0;
+  if (B.w > 0) {
+    const MmaSeg& S0 = segs[B.z];
+    zmin_n = S0.zmin;
+    ulen_n = S0.ulen;
+    if (grow) {
+      lo_n = S0.lo[g];
+      hi_n = S0.hi[g];
+      vb_n = S0.vb[g];
+    }
+  }
   pdl_wait();
   const TileRec* tr = T.rec + ti;
   const int M = T.M, m = tr->m;
@@ -342,18 +359,25 @@ __global__ void __launch_bounds__(256) k_fwd_pull_mma(SolveArgs A, TileArg T, co
   bool any = false;  // a tile without an active member does nothing (CTA-uniform)
   for (int k = 0; k < M; ++k) any |= (A.flag[tr->t[k]] != 0) == (A.flag_on != 0);
   if (!any) return;
-  const int4 B = blk[b];  // (first item, rows, first segment, segments)
-  const int g = lane >> 2, q = lane & 3;
   const cplx* vals = A.vals + (long long)tr->c * A.nvals;
   const cplx* X = A.X + cb;
   double cr[NB][2], ci[NB][2];
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb) cr[nb][0] = cr[nb][1] = ci[nb][0] = ci[nb][1] = 0.0;
   for (int u = B.z; u < B.z + B.w; ++u) {
-    const MmaSeg& S = segs[u];
-    const int zmin = S.zmin, ulen = S.ulen;
-    const int lo = g < B.y ? S.lo[g] : 0, hi = g < B.y ? S.hi[g] : 0;
-    const cplx* vrow = vals + (g < B.y ? S.vb[g] : 0);
+    // this segment's record was loaded one iteration ahead; the next one's goes out now
+    const int zmin = zmin_n, ulen = ulen_n, lo = lo_n, hi = hi_n;
+    const cplx* vrow = vals + vb_n;
+    if (u + 1 < B.z + B.w) {
+      const MmaSeg& S = segs[u + 1];
+      zmin_n = S.zmin;
+      ulen_n = S.ulen;
+      if (grow) {
+        lo_n = S.lo[g];
+        hi_n = S.hi[g];
+        vb_n = S.vb[g];
+      }
+    }
     for (int k0 = 4 * wp; k0 < ulen; k0 += 32) {
       const int z = zmin + k0 + q;
       const bool zin = k0 + q < ulen;
