@@ -1067,8 +1067,10 @@ void hddm_engine::build_plan() {
       L.nmblk = int(blks.size());
       L.d_mblk = upload(blks);
     }
-    L.split_rows = rows > 64L * long(sns.size());  // long row lists
-    L.split_diag = nmax > 48;
+    static const long split_rows_min = std::getenv("HDDM_SPLIT_ROWS_MIN") ? std::atol(std::getenv("HDDM_SPLIT_ROWS_MIN")) : 64;
+    static const long split_diag_min = std::getenv("HDDM_SPLIT_DIAG_MIN") ? std::atol(std::getenv("HDDM_SPLIT_DIAG_MIN")) : 12;
+    L.split_rows = rows > split_rows_min * long(sns.size());  // long row lists
+    L.split_diag = nmax > split_diag_min;
     if (env_sr) L.split_rows = std::atoi(env_sr) != 0;
     if (env_sd) L.split_diag = std::atoi(env_sd) != 0;
     if (L.split_rows || L.split_diag)
