@@ -131,7 +131,7 @@ struct hddm_engine {
   int* d_act_list = nullptr;
   long long* d_counts = nullptr;
   double* d_part_chk = nullptr;
-  int nchunk = std::getenv("HDDM_CHECK_CHUNKS") ? std::atoi(std::getenv("HDDM_CHECK_CHUNKS")) : 64;  // residual-check partials per subdomain
+  int nchunk = std::getenv("HDDM_CHECK_CHUNKS") ? std::atoi(std::getenv("HDDM_CHECK_CHUNKS")) : 32;  // residual-check partials per subdomain
   double* d_rel = nullptr;
   int* d_refine = nullptr;
   double* d_maxrel = nullptr;

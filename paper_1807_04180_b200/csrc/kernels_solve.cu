@@ -1092,20 +1092,21 @@ static int pow2_floor(long v) {
 }
 
 // lanes per output for a forward pull/diagonal level with mean inner length avg
-// (defaults measured best at config 4; tuning knobs HDDM_FWD_DIV / HDDM_FWD_WIDE)
-// Two parameter sets: the full-RHS plan (step 1, class solves; measured best at
-// config 4 with the full forward: HDDM_FWD_DIV 32, HDDM_FWD_WIDE 16) and the
-// steady-state sparse-RHS plan of steps >= 2 (config 4: HDDM_FWD_DIV_SP 16 against 32,
-// 1.81 -> 1.75 ms per step; per-level tuning with tools/tune_fwd_shapes.py finds no
-// better point).
+// (tuning knobs HDDM_FWD_DIV / HDDM_FWD_WIDE). Two parameter sets: the full-RHS plan
+// (step 1, class solves, refinement corrections) and the steady-state sparse-RHS plan of
+// steps >= 2. Singleton tiles take E = avg / div lanes per row: re-measured on the round's
+// final kernels (tools/run42.sh, run43.sh) div = 16 (full), 8 (sparse) and 2 for the inverse
+// rows -- twice the lanes of the round-1 values: config 3 step 1.632 -> 1.414 ms, config 1
+// 0.451 -> 0.383, config 2 0.721 -> 0.705; config 4 (member tiles: E from HDDM_FWD_WIDE)
+// does not move, and per-level tuning (tools/tune_fwd_shapes.py) found no better point.
 static long env_long(const char* name, long dflt) {
   const char* v = std::getenv(name);
   return v ? std::atol(v) : dflt;
 }
 
 static int fwd_lanes(int M, long avg, bool diag = false, bool sparse = false) {
-  static const long div_pull = env_long("HDDM_FWD_DIV", 32), div_pull_sp = env_long("HDDM_FWD_DIV_SP", 16);
-  static const long div_diag = env_long("HDDM_DIAG_DIV", 4);
+  static const long div_pull = env_long("HDDM_FWD_DIV", 16), div_pull_sp = env_long("HDDM_FWD_DIV_SP", 8);
+  static const long div_diag = env_long("HDDM_DIAG_DIV", 2);
   static const long wide = env_long("HDDM_FWD_WIDE", 16), wide_sp = env_long("HDDM_FWD_WIDE_SP", 6);
   const long div = diag ? div_diag : (sparse ? div_pull_sp : div_pull);
   if (M == 1) return std::max(1, std::min(32, pow2_floor(avg / div)));
