@@ -802,9 +802,12 @@ void hddm_engine::build_plan() {
     // 4 tiles per group measured best at config 4 (more, shorter launch chains
     // overlap better; 1 per group is launch-bound)
     const char* cap_env = std::getenv("HDDM_GROUP_TILES");
-    const int cap = cap_env ? std::max(1, std::atoi(cap_env)) : 4;
+    const int cap1 = cap_env ? std::max(1, std::atoi(cap_env)) : 4;
+    const char* capm_env = std::getenv("HDDM_GROUP_TILES_M");  // groups of multi-member tiles
+    const int capm = capm_env ? std::max(1, std::atoi(capm_env)) : cap1;
     for (auto& kv : byM) {
       const int M = kv.first;
+      const int cap = M > 1 ? capm : cap1;
       if (std::find(Rs.begin(), Rs.end(), 32 / M) == Rs.end()) Rs.push_back(32 / M);
       for (size_t a = 0; a < kv.second.size(); a += cap) {
         const size_t b = std::min(kv.second.size(), a + size_t(cap));
