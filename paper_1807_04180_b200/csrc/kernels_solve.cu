@@ -1041,8 +1041,10 @@ __global__ void __launch_bounds__(512) k_sep_trsv(SolveArgs A, TileArg T, const 
   }
 }
 
-static bool g_dry = false;  // count the launches of a solve without launching (solve_launch_count)
-static int g_count = 0;
+// count the launches of a solve without launching (solve_launch_count); per host thread,
+// so a dry run never swallows another thread's launches
+static thread_local bool g_dry = false;
+static thread_local int g_count = 0;
 
 template <bool BWD>
 static void launch_sep_trsv(const SolveArgs& A, const TileArg& T, const SolveLevel& L, cudaStream_t st) {
@@ -1059,7 +1061,7 @@ static void launch_sep_trsv(const SolveArgs& A, const TileArg& T, const SolveLev
 }
 
 // ------------------------------------------------------------------ launcher
-static bool g_pdl = false;   // the chain being enqueued (SolvePlan::pdl)
+static thread_local bool g_pdl = false;   // the chain being enqueued (SolvePlan::pdl)
 
 // launch with programmatic stream serialization (see pdl_trigger / pdl_wait)
 template <typename... KArgs, typename... Args>
